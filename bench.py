@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""Benchmark of the VND hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c3|c2|c4]
+
+Workload (BASELINE.json configs[2], the config the metric "neighbor
+evals/sec & VND time-to-local-opt at 1/2/4/8 B200" is quoted on): the
+seed-0 synthetic instance K=100,000 products x T=52 periods, VND (N1..N4) to
+the local optimum from the lot-for-lot start.  A step is one full descent.
+Under torchrun the products are sharded in contiguous blocks across ranks
+(strong scaling, no data-path collective; one all-reduce of the totals).
+
+value   = reference-equivalent neighbor evaluations (the reference's lockstep
+          count) per second, whole job, inputs resident.
+e2e     = same metric through the C ABI with host (pinned) buffers: every
+          step re-uploads the instance and the start plan and reads back the
+          final plan, trace and stats.
+--impl reference = the CPU reference path (oracle/, a C restatement of the
+          reference's numba kernels run product-parallel on every host core)
+          on a bounded sample of the same instance.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c3": dict(products=100_000, periods=52, name="K=100000 T=52 seed0 VND-to-local-opt"),
+    "c2": dict(products=1_000, periods=52, name="K=1000 T=52 seed0 VND-to-local-opt"),
+    "c4": dict(products=10_000, periods=520, name="K=10000 T=520 seed0 VND-to-local-opt"),
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sms, maxes, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxes.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": max(maxes),
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_reference(inst, sample_products, steps, warmup, threads):
+    """Time the CPU reference path (oracle port) on the first products."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    oracle.lib()
+    sub = inst.slice(0, sample_products)
+    oi = oracle.OracleInstance(sub)
+    sm, sr = oracle.initial_solution(oi)
+    times, stats = [], None
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        _, _, cost, _, stats = oracle.vnd(oi, sm, sr, 4, threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    t = float(np.mean(times))
+    return dict(value=stats["evals"] / t, evals=stats["evals"], seconds_per_step=t, cost=cost,
+                sweeps=stats["sweeps"])
+
+
+def int32_peak(torch, ext):
+    """Measured INT32 add throughput (ops/s) of this GPU (rl microbench)."""
+    return ext.int_peak()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-sample", type=int, default=20000,
+                    help="products of the instance timed on the CPU baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    wl = WORKLOADS[args.workload]
+    from paper_1704_05132_b200.model import GeneratorConfig, generate_instance
+
+    threads = len(os.sched_getaffinity(0))
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        inst = generate_instance(GeneratorConfig(products=wl["products"], periods=wl["periods"],
+                                                 seed=0))
+        sample = min(args.cpu_sample, wl["products"])
+        r = cpu_reference(inst, sample, args.steps, args.warmup, threads)
+        line = {
+            "impl": "reference", "metric": "neighbor evals/sec (reference-equivalent)",
+            "value": r["value"], "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["seconds_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic (reference generator, seed 0)",
+            "config": {"workload": wl["name"], "products": wl["products"],
+                       "periods": wl["periods"], "k_max": 4, "parallelism": "cpu-threads"},
+            "cpu_baseline": {"value": r["value"], "unit": "evals/s", "cores": threads,
+                             "kind": "port",
+                             "sample": f"first {sample} products of the workload instance, "
+                                       "lockstep VND to local optimum (oracle/remlot_oracle.c, "
+                                       "pthreads product-parallel)"},
+            "e2e": {"value": r["value"], "unit": "evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "sample_evals_per_step": r["evals"], "sample_cost": r["cost"],
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    from paper_1704_05132_b200 import _native
+    from paper_1704_05132_b200 import devbench
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    K, T = wl["products"], wl["periods"]
+    inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=0))
+    lo, hi = K * rank // world, K * (rank + 1) // world
+    shard = inst.slice(lo, hi)
+    dev = _native.DeviceInstance(shard)
+    stream = torch.cuda.Stream()   # a real stream: events and kernels share it
+    torch.cuda.set_stream(stream)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    Ks = hi - lo
+    plan = torch.empty((4, Ks, T), dtype=torch.uint8, device="cuda")
+    _native.check(_native.load().rl_initial_solution_device(
+        dev.h, ctypes.c_void_p(plan[0].data_ptr()), ctypes.c_void_p(plan[1].data_ptr()), sptr),
+        "rl_initial_solution_device")
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def step():
+        _native.check(_native.load().rl_vnd_device(
+            dev.h, 4, ctypes.c_void_p(plan[0].data_ptr()), ctypes.c_void_p(plan[1].data_ptr()),
+            ctypes.c_void_p(plan[2].data_ptr()), ctypes.c_void_p(plan[3].data_ptr()), sptr),
+            "rl_vnd_device")
+
+    def collect():
+        tr = np.empty(1 << 16, np.int64)
+        nt = np.zeros(1, np.int64)
+        st = np.zeros(8, np.int64)
+        _native.check(_native.load().rl_vnd_collect(dev.h, _native.ptr(tr), len(tr),
+                                                    _native.ptr(nt), _native.ptr(st)),
+                      "rl_vnd_collect")
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = collect()
+    # ---- timed region (device): per-step CUDA events, L2 flushed between steps
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    launches0 = dev.launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    kernel_ms = []
+    for e0, e1 in evs:
+        flush.zero_()
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        kernel_ms.append(collect()[7] / 1e6)
+    torch.cuda.synchronize()
+    launches = dev.launches - launches0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    my_ms = float(np.sum(step_ms))
+    st = collect()
+    # totals across ranks: time = max, work = sum
+    tot = torch.tensor([st[4], st[3], st[0], st[5], st[2]], dtype=torch.int64, device="cuda")
+    tmax = torch.tensor([my_ms, float(np.mean(kernel_ms))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ref_evals, done_evals, final_cost, moves, _ = [int(x) for x in tot.tolist()]
+    total_ms, vnd_kernel_ms = tmax.tolist()
+    ms_per_step = total_ms / args.steps
+
+    # ---- e2e through the C ABI with pinned host buffers
+    e2e_ms, h2d, d2h = devbench.e2e_steps(torch, _native, dev, shard, args.steps, world, dist)
+
+    line = None
+    if rank == 0:
+        value = ref_evals * args.steps / (total_ms / 1e3)
+        peak_ops = devbench.int32_peak_ops()
+        alg_ops = done_evals * 8 * T / world   # 8T int ops per evaluation
+        achieved = alg_ops / (vnd_kernel_ms / 1e3)
+        line = {
+            "metric": "neighbor evals/sec (reference-equivalent) & VND time-to-local-opt",
+            "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "time_to_local_opt_ms": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int32/int64 (exact integer cents)",
+            "data": "synthetic (reference generator model.py:115-153, seed 0)",
+            "config": {"workload": wl["name"], "products": K, "periods": T, "k_max": 4,
+                       "parallelism": f"product-shard x{world}",
+                       "l2": "flushed between steps (256 MiB write)",
+                       "cost_type_bytes": dev.info["cost_bytes"],
+                       "value_type_bytes": dev.info["value_bytes"]},
+            "evals_reference_per_step": ref_evals, "evals_performed_per_step": done_evals,
+            "performed_evals_per_s": done_evals * args.steps / (total_ms / 1e3),
+            "final_cost": final_cost, "moves_per_step": moves,
+            "gpu_launches": int(launches) * world,
+            "clocks": clocks,
+            "e2e": {"value": ref_evals * args.steps / (e2e_ms / 1e3), "unit": "evals/s",
+                    "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "int_alu", "kernel": "k_vnd",
+                         "achieved": achieved / 1e9, "peak": peak_ops / 1e9,
+                         "unit": "Gop/s", "frac": achieved / peak_ops,
+                         "peak_source": "INT32 add microbenchmark run in this bench",
+                         "ops_definition": "8*T int ops per performed neighbor evaluation "
+                                           "(SURVEY.md 8(d))",
+                         "kernel_ms": vnd_kernel_ms, "traffic": None},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            # bounded sample sized for ~10-20 s of CPU work on this host
+            probe = cpu_reference(inst, min(1000, K), 1, 0, threads)
+            per_product = probe["seconds_per_step"] / min(1000, K)
+            sample = int(min(K, max(1000, 12.0 / max(per_product, 1e-9))))
+            r = cpu_reference(inst, sample, 1, 0, threads)
+            line["cpu_baseline"] = {
+                "value": r["value"], "unit": "evals/s", "cores": threads, "kind": "port",
+                "sample": f"first {sample} products, lockstep VND to local optimum "
+                          f"({r['seconds_per_step']:.2f} s)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

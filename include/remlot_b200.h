@@ -1,0 +1,127 @@
+/*
+ * remlot_b200.h -- C ABI of the B200 VND hot path (libremlot_b200.so).
+ *
+ * Drop-in boundary for the reference package `remlot`, whose operator API is
+ * its set of numba kernels called with flat numpy buffers
+ * (reference pkg/src/remlot/_kernels.py) plus the VND driver (vnd.py).  Each
+ * entry point below names the reference interface it replaces.  Plain C
+ * types only: host pointers unless the name ends in _device (device
+ * pointers, asynchronous on the given cudaStream_t passed as void*).
+ *
+ * Conventions (mirroring the reference):
+ *   - setup plans are two bool (uint8 0/1) K x T C-order matrices;
+ *   - instance matrices are int64 K x T C-order; cost vectors int64[K] in the
+ *     order setup_m, setup_r, holding_m, holding_r, unit_m, unit_r;
+ *   - costs are int64 cents, RL_INFEASIBLE = 1 << 62 (_kernels.py:11);
+ *   - caller-allocated outputs; return 0 on success, negative on error
+ *     (RL_E*), message in rl_last_error() (thread-local);
+ *   - a handle is bound to the CUDA device that was current at creation;
+ *     calls on one handle must not overlap (one handle per thread/stream).
+ */
+#ifndef REMLOT_B200_H
+#define REMLOT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RL_INFEASIBLE ((int64_t)1 << 62)
+
+#define RL_OK 0
+#define RL_EINVAL -1   /* bad argument (reference raises ValueError/IndexError) */
+#define RL_ECUDA -2    /* CUDA runtime error (message says which) */
+#define RL_ERANGE -4   /* instance values outside the exact int64 range */
+
+typedef struct rl_instance rl_instance;
+
+/* Upload an instance once; the handle owns its device memory.
+ * Replaces the Instance arrays handed to every kernel call
+ * (reference model.py:28-72, vnd.py:141-145, plan.py:120-123). */
+int rl_instance_create(int64_t K, int64_t T, const int64_t *demand, const int64_t *returns,
+                       const int64_t *setup_m, const int64_t *setup_r,
+                       const int64_t *hold_m, const int64_t *hold_r,
+                       const int64_t *unit_m, const int64_t *unit_r, rl_instance **out);
+/* Re-upload new data of the same K x T into an existing handle. */
+int rl_instance_update(rl_instance *h, const int64_t *demand, const int64_t *returns,
+                       const int64_t *setup_m, const int64_t *setup_r,
+                       const int64_t *hold_m, const int64_t *hold_r,
+                       const int64_t *unit_m, const int64_t *unit_r);
+void rl_instance_destroy(rl_instance *h);
+/* info[0..5] = K, T, bytes per period value (4|8), bytes per cost (4|8),
+ * SM count, warps per CTA of the resident VND kernel. */
+int rl_instance_info(const rl_instance *h, int64_t *info);
+
+/* _kernels.product_costs(lo, hi, ...) (_kernels.py:171-175) / plan.evaluate
+ * (plan.py:117-126): out[k] for k in [lo, hi), RL_INFEASIBLE if infeasible.
+ * sm/sr are full K x T plans; out has K entries. */
+int rl_product_costs(rl_instance *h, int64_t lo, int64_t hi, const uint8_t *sm,
+                     const uint8_t *sr, int64_t *out);
+
+/* _kernels.scan_products(lo, hi, ..., nbh, out_*) (_kernels.py:261-325):
+ * best strictly improving move of neighborhood nbh per product in [lo, hi);
+ * out_* have K entries, only [lo, hi) is written.  m0/r0 (m1/r1) are 0 where
+ * no move won (where p1 < 0); the reference leaves them unwritten.
+ * *evals (may be NULL) = number of candidate moves scored. */
+int rl_scan_products(rl_instance *h, int64_t lo, int64_t hi, const uint8_t *sm,
+                     const uint8_t *sr, int nbh, int64_t *dec, int64_t *p0, uint8_t *m0,
+                     uint8_t *r0, int64_t *p1, uint8_t *m1, uint8_t *r1, int64_t *evals);
+
+/* _kernels.apply_scan(lo, hi, ...) (_kernels.py:328-344): writes winners into
+ * sm/sr (K x T, in place) and returns the product-ordered sum in *diff. */
+int rl_apply_scan(rl_instance *h, int64_t lo, int64_t hi, const int64_t *dec,
+                  const int64_t *p0, const uint8_t *m0, const uint8_t *r0, const int64_t *p1,
+                  const uint8_t *m1, const uint8_t *r1, uint8_t *sm, uint8_t *sr,
+                  int64_t *diff);
+
+/* _kernels.list_moves(nbh, sm_row, sr_row, mp0, mm0, mr0, mp1, mm1, mr1)
+ * (_kernels.py:188-258) for one product row of length T; buffers hold 2T
+ * entries; *n = move count.  mm1/mr1 are 0 for single-period moves. */
+int rl_list_moves(int nbh, int64_t T, const uint8_t *sm_row, const uint8_t *sr_row,
+                  int64_t *mp0, uint8_t *mm0, uint8_t *mr0, int64_t *mp1, uint8_t *mm1,
+                  uint8_t *mr1, int64_t *n);
+
+/* vnd.vnd(inst, plan, k_max) (vnd.py:253-289): descend to a local optimum of
+ * N1..Nk_max.  Bit-identical plan, cost and trace to the reference's
+ * lockstep loop.  trace gets 1 + k_max*sweeps entries (*n_trace; if it
+ * exceeds trace_cap only trace_cap are written).  stats[0..7] = final cost,
+ * start cost, sweeps, candidate evaluations performed, reference-equivalent
+ * evaluations (lockstep count), moves applied, products,
+ * kernel time in ns. */
+int rl_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t *sr_in,
+           uint8_t *sm_out, uint8_t *sr_out, int64_t *trace, int64_t trace_cap,
+           int64_t *n_trace, int64_t *stats);
+
+/* Device-resident variant: plans are device pointers; enqueued on stream
+ * (cudaStream_t as void*, NULL = the handle's stream) without host sync.
+ * Read results with rl_vnd_collect afterwards. */
+int rl_vnd_device(rl_instance *h, int k_max, const uint8_t *d_sm_in, const uint8_t *d_sr_in,
+                  uint8_t *d_sm_out, uint8_t *d_sr_out, void *stream);
+int rl_vnd_collect(rl_instance *h, int64_t *trace, int64_t trace_cap, int64_t *n_trace,
+                   int64_t *stats);
+
+/* plan.initial_solution(inst) (plan.py:140-167): lot-for-lot start. */
+int rl_initial_solution(rl_instance *h, uint8_t *sm, uint8_t *sr);
+int rl_initial_solution_device(rl_instance *h, uint8_t *d_sm, uint8_t *d_sr, void *stream);
+
+/* plan.decode (plan.py:99-114, _kernels.row_decode :100-168): per period
+ * quantities x_m, x_r and stocks y_m, y_r (K x T each) and per product cost;
+ * rows of infeasible products are zero and their cost RL_INFEASIBLE. */
+int rl_decode(rl_instance *h, const uint8_t *sm, const uint8_t *sr, int64_t *x_m,
+              int64_t *x_r, int64_t *y_m, int64_t *y_r, int64_t *cost);
+
+/* Measured INT32 throughput of the current device (integer ops/s; IMAD +
+ * LOP3 chains over all SMs): the roofline denominator of the ALU-bound VND
+ * kernel. */
+int rl_int_peak(double *ops_per_s);
+
+/* Number of kernel launches issued by this handle since creation. */
+int64_t rl_launch_count(const rl_instance *h);
+
+const char *rl_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

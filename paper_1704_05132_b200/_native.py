@@ -1,0 +1,226 @@
+"""ctypes binding of libremlot_b200.so (the C ABI in include/remlot_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA
+device is visible, every call raises.  The library is built in-tree by
+``paper_1704_05132_b200.build`` (nvcc, sm_100a) into ``_lib/``.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("REMLOT_B200_LIB") or os.path.join(HERE, "_lib", "libremlot_b200.so")
+INFEASIBLE = 1 << 62
+
+RL_EINVAL = -1
+RL_ECUDA = -2
+RL_ERANGE = -4
+
+# every symbol include/remlot_b200.h declares (checked by tests/test_native_lib.py)
+EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
+           "rl_instance_info", "rl_product_costs", "rl_scan_products", "rl_apply_scan",
+           "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect",
+           "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_int_peak", "rl_launch_count",
+           "rl_last_error")
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def load():
+    """Load the library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    I = ctypes.c_int
+    I64 = ctypes.c_int64
+    sig = {
+        "rl_instance_create": (I, [I64, I64] + [P] * 8 + [ctypes.POINTER(P)]),
+        "rl_instance_update": (I, [P] + [P] * 8),
+        "rl_instance_destroy": (None, [P]),
+        "rl_instance_info": (I, [P, P]),
+        "rl_product_costs": (I, [P, I64, I64, P, P, P]),
+        "rl_scan_products": (I, [P, I64, I64, P, P, I] + [P] * 8),
+        "rl_apply_scan": (I, [P, I64, I64] + [P] * 10),
+        "rl_list_moves": (I, [I, I64] + [P] * 9),
+        "rl_vnd": (I, [P, I, P, P, P, P, P, I64, P, P]),
+        "rl_vnd_device": (I, [P, I, P, P, P, P, P]),
+        "rl_vnd_collect": (I, [P, P, I64, P, P]),
+        "rl_initial_solution": (I, [P, P, P]),
+        "rl_initial_solution_device": (I, [P, P, P, P]),
+        "rl_decode": (I, [P] + [P] * 7),
+        "rl_int_peak": (I, [P]),
+        "rl_launch_count": (I64, [P]),
+        "rl_last_error": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc, what):
+    if rc == 0:
+        return
+    msg = load().rl_last_error().decode(errors="replace")
+    if rc in (RL_EINVAL, RL_ERANGE):
+        raise ValueError(f"{what}: {msg}")
+    raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def u8(a):
+    """Bool/uint8 K x T plan matrix as a contiguous uint8 view (no copy if possible)."""
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.bool_:
+        return a.view(np.uint8)
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+class DeviceInstance:
+    """Device-resident copy of an Instance (owns an rl_instance handle)."""
+
+    def __init__(self, inst):
+        lib = load()
+        self.K = int(inst.products)
+        self.T = int(inst.periods)
+        arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in inst.arrays()]
+        h = ctypes.c_void_p()
+        check(lib.rl_instance_create(self.K, self.T, *[ptr(a) for a in arrays],
+                                     ctypes.byref(h)), "rl_instance_create")
+        self.h = h
+        info = np.zeros(6, np.int64)
+        check(lib.rl_instance_info(h, ptr(info)), "rl_instance_info")
+        self.info = dict(K=int(info[0]), T=int(info[1]), value_bytes=int(info[2]),
+                         cost_bytes=int(info[3]), sms=int(info[4]), warps_per_cta=int(info[5]))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None:
+            _lib.rl_instance_destroy(h)
+            self.h = None
+
+    @property
+    def launches(self):
+        return int(load().rl_launch_count(self.h))
+
+    def update(self, inst):
+        arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in inst.arrays()]
+        check(load().rl_instance_update(self.h, *[ptr(a) for a in arrays]),
+              "rl_instance_update")
+
+    def product_costs(self, sm, sr, lo=0, hi=None):
+        hi = self.K if hi is None else hi
+        sm, sr = u8(sm), u8(sr)
+        out = np.zeros(self.K, np.int64)
+        check(load().rl_product_costs(self.h, lo, hi, ptr(sm), ptr(sr), ptr(out)),
+              "rl_product_costs")
+        return out
+
+    def scan_products(self, sm, sr, nbh, lo=0, hi=None):
+        """Returns ((dec, p0, m0, r0, p1, m1, r1), evals) like _kernels.scan_products."""
+        hi = self.K if hi is None else hi
+        sm, sr = u8(sm), u8(sr)
+        K = self.K
+        dec = np.zeros(K, np.int64)
+        p0 = np.full(K, -1, np.int64)
+        p1 = np.full(K, -1, np.int64)
+        b = [np.zeros(K, np.uint8) for _ in range(4)]
+        ev = np.zeros(1, np.int64)
+        check(load().rl_scan_products(self.h, lo, hi, ptr(sm), ptr(sr), nbh, ptr(dec), ptr(p0),
+                                      ptr(b[0]), ptr(b[1]), ptr(p1), ptr(b[2]), ptr(b[3]),
+                                      ptr(ev)), "rl_scan_products")
+        return (dec, p0, b[0].view(np.bool_), b[1].view(np.bool_), p1, b[2].view(np.bool_),
+                b[3].view(np.bool_)), int(ev[0])
+
+    def apply_scan(self, out, sm, sr, lo=0, hi=None):
+        hi = self.K if hi is None else hi
+        dec, p0, m0, r0, p1, m1, r1 = out
+        sm8, sr8 = u8(sm), u8(sr)
+        i64 = [np.ascontiguousarray(a, np.int64) for a in (dec, p0, p1)]
+        b = [u8(a) for a in (m0, r0, m1, r1)]
+        diff = np.zeros(1, np.int64)
+        check(load().rl_apply_scan(self.h, lo, hi, ptr(i64[0]), ptr(i64[1]), ptr(b[0]),
+                                   ptr(b[1]), ptr(i64[2]), ptr(b[2]), ptr(b[3]), ptr(sm8),
+                                   ptr(sr8), ptr(diff)), "rl_apply_scan")
+        return int(diff[0])
+
+    def vnd(self, sm, sr, k_max=4, trace_cap=None):
+        """Returns (sm, sr, trace, stats) with stats a dict."""
+        sm, sr = u8(sm), u8(sr)
+        out_m = np.empty((self.K, self.T), np.bool_)
+        out_r = np.empty((self.K, self.T), np.bool_)
+        cap = trace_cap or 4096
+        while True:
+            trace = np.empty(cap, np.int64)
+            nt = np.zeros(1, np.int64)
+            st = np.zeros(8, np.int64)
+            check(load().rl_vnd(self.h, k_max, ptr(sm), ptr(sr), ptr(out_m.view(np.uint8)),
+                                ptr(out_r.view(np.uint8)), ptr(trace), cap, ptr(nt), ptr(st)),
+                  "rl_vnd")
+            if nt[0] <= cap:
+                break
+            cap = int(nt[0])
+        stats = dict(cost=int(st[0]), start_cost=int(st[1]), sweeps=int(st[2]),
+                     evals=int(st[3]), evals_reference=int(st[4]), moves=int(st[5]),
+                     products=int(st[6]), kernel_ns=int(st[7]))
+        return out_m, out_r, trace[:nt[0]].copy(), stats
+
+    def decode(self, sm, sr):
+        sm, sr = u8(sm), u8(sr)
+        outs = [np.zeros((self.K, self.T), np.int64) for _ in range(4)]
+        cost = np.zeros(self.K, np.int64)
+        check(load().rl_decode(self.h, ptr(sm), ptr(sr), *[ptr(o) for o in outs], ptr(cost)),
+              "rl_decode")
+        return outs[0], outs[1], outs[2], outs[3], cost
+
+    def initial_solution(self):
+        sm = np.empty((self.K, self.T), np.bool_)
+        sr = np.empty((self.K, self.T), np.bool_)
+        check(load().rl_initial_solution(self.h, ptr(sm.view(np.uint8)), ptr(sr.view(np.uint8))),
+              "rl_initial_solution")
+        return sm, sr
+
+
+def list_moves(nbh, sm_row, sr_row):
+    sm_row, sr_row = u8(sm_row), u8(sr_row)
+    T = len(sm_row)
+    cap = 2 * T + 2
+    mp0 = np.zeros(cap, np.int64)
+    mp1 = np.zeros(cap, np.int64)
+    b = [np.zeros(cap, np.uint8) for _ in range(4)]
+    n = np.zeros(1, np.int64)
+    check(load().rl_list_moves(nbh, T, ptr(sm_row), ptr(sr_row), ptr(mp0), ptr(b[0]),
+                               ptr(b[1]), ptr(mp1), ptr(b[2]), ptr(b[3]), ptr(n)),
+          "rl_list_moves")
+    c = int(n[0])
+    return (mp0[:c], b[0][:c].view(np.bool_), b[1][:c].view(np.bool_), mp1[:c],
+            b[2][:c].view(np.bool_), b[3][:c].view(np.bool_))
+
+
+def device_instance(inst):
+    """The cached DeviceInstance of ``inst`` (uploaded once per Instance)."""
+    dev = getattr(inst, "_device", None)
+    if dev is None:
+        dev = DeviceInstance(inst)
+        try:
+            inst._device = dev
+        except AttributeError:
+            pass
+    return dev

@@ -1,0 +1,71 @@
+"""Measurement helpers for bench.py (device peaks and the end-to-end leg)."""
+
+import ctypes
+import time
+
+import numpy as np
+
+
+def int32_peak_ops():
+    """Measured INT32 op/s of the current GPU (rl_int_peak microbenchmark)."""
+    from . import _native
+    out = np.zeros(1, np.float64)
+    _native.check(_native.load().rl_int_peak(_native.ptr(out)), "rl_int_peak")
+    return float(out[0])
+
+
+def _pinned(torch, a):
+    t = torch.empty(a.shape, dtype={np.int64: torch.int64, np.uint8: torch.uint8,
+                                    np.bool_: torch.uint8}[a.dtype.type], pin_memory=True)
+    arr = t.numpy()
+    arr[...] = a
+    return t, arr
+
+
+def e2e_steps(torch, _native, dev, shard, steps, world, dist):
+    """Time `steps` end-to-end descents through the C ABI with pinned host
+    buffers: each step uploads the instance (rl_instance_update) and the
+    start plan, runs the VND (rl_vnd) and reads back the final plan, trace
+    and stats.  Returns (max-over-ranks total ms, h2d bytes, d2h bytes) for
+    the whole job."""
+    lib = _native.load()
+    keep = []
+    arrays = []
+    for a in shard.arrays():
+        t, arr = _pinned(torch, np.ascontiguousarray(a, np.int64))
+        keep.append(t)
+        arrays.append(arr)
+    sm0, sr0 = dev.initial_solution()
+    tm, sm = _pinned(torch, sm0.view(np.uint8))
+    tr_, sr = _pinned(torch, sr0.view(np.uint8))
+    to, om = _pinned(torch, np.zeros_like(sm))
+    tq, orr = _pinned(torch, np.zeros_like(sr))
+    keep += [tm, tr_, to, tq]
+    trace = np.empty(1 << 16, np.int64)
+    nt = np.zeros(1, np.int64)
+    st = np.zeros(8, np.int64)
+    P = _native.ptr
+
+    def one():
+        _native.check(lib.rl_instance_update(dev.h, *[P(a) for a in arrays]),
+                      "rl_instance_update")
+        _native.check(lib.rl_vnd(dev.h, 4, P(sm), P(sr), P(om), P(orr), P(trace), len(trace),
+                                 P(nt), P(st)), "rl_vnd")
+
+    one()   # warm
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    h2d = sum(a.nbytes for a in arrays) + sm.nbytes + sr.nbytes
+    d2h = om.nbytes + orr.nbytes + int(nt[0]) * 8 + st.nbytes + 24
+    tot = torch.tensor([ms, 0.0], dtype=torch.float64, device="cuda")
+    byt = torch.tensor([h2d, d2h], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        dist.all_reduce(byt, op=dist.ReduceOp.SUM)
+    return float(tot[0]), int(byt[0]), int(byt[1])

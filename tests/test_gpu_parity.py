@@ -1,0 +1,278 @@
+"""CUDA path vs the reference: golden fixtures made by the live reference
+(tests/golden/) and the CPU oracle (oracle/), bit-exact integer equality.
+
+Every call goes through the C ABI (libremlot_b200.so via ctypes)."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, GoldInstance, golden
+from paper_1704_05132_b200 import (GeneratorConfig, Instance, generate_instance,
+                                   initial_solution)
+from paper_1704_05132_b200._native import DeviceInstance, list_moves
+
+pytestmark = pytest.mark.gpu
+NAMES = ("dec", "p0", "m0", "r0", "p1", "m1", "r1")
+
+
+def _inst(g):
+    return Instance(g.products, g.periods, g.demand, g.returns, g.setup_cost_m,
+                    g.setup_cost_r, g.holding_cost_m, g.holding_cost_r, g.unit_cost_m,
+                    g.unit_cost_r)
+
+
+def _plan_sha(sm, sr):
+    h = hashlib.sha256()
+    h.update(np.packbits(np.asarray(sm, bool)).tobytes())
+    h.update(np.packbits(np.asarray(sr, bool)).tobytes())
+    return h.hexdigest()
+
+
+def _cases(small_cases):
+    for idx, K, T in small_cases["cases"]:
+        inst = _inst(GoldInstance(small_cases, f"c{idx}_"))
+        dev = DeviceInstance(inst)
+        for pi in range(int(small_cases["n_plans"])):
+            yield inst, dev, f"c{idx}_{pi}_"
+
+
+def test_product_costs_golden(small_cases):
+    for inst, dev, p in _cases(small_cases):
+        got = dev.product_costs(small_cases[p + "sm"], small_cases[p + "sr"])
+        np.testing.assert_array_equal(got, small_cases[p + "cost"], err_msg=p)
+
+
+def test_list_moves_golden(small_cases):
+    for inst, dev, p in _cases(small_cases):
+        sm, sr = small_cases[p + "sm"], small_cases[p + "sr"]
+        for nbh in (1, 2, 3, 4):
+            ns = small_cases[p + f"lm{nbh}_n"]
+            for k in range(min(inst.products, 3)):
+                got = list_moves(nbh, sm[k], sr[k])
+                n = int(ns[k])
+                assert len(got[0]) == n
+                for name, g in zip(("mp0", "mm0", "mr0", "mp1", "mm1", "mr1"), got):
+                    np.testing.assert_array_equal(g, small_cases[p + f"lm{nbh}_{name}"][k, :n])
+
+
+def test_scan_products_golden(small_cases):
+    for inst, dev, p in _cases(small_cases):
+        for nbh in (1, 2, 3, 4):
+            out, ev = dev.scan_products(small_cases[p + "sm"], small_cases[p + "sr"], nbh)
+            dec = out[0]
+            for name, g in zip(NAMES, out):
+                g = np.array(g)
+                if name in ("m0", "r0"):
+                    g &= dec > 0
+                if name in ("m1", "r1"):
+                    g &= (dec > 0) & (out[4] >= 0)
+                np.testing.assert_array_equal(g, small_cases[p + f"scan{nbh}_{name}"],
+                                              err_msg=f"{p} nbh={nbh} {name}")
+            _, oev = oracle.scan_products(inst, small_cases[p + "sm"], small_cases[p + "sr"], nbh)
+            assert ev == oev
+
+
+def test_vnd_golden(small_cases):
+    for inst, dev, p in _cases(small_cases):
+        for k_max in (1, 4):
+            sm, sr, trace, st = dev.vnd(small_cases[p + "sm"], small_cases[p + "sr"], k_max)
+            assert st["cost"] == int(small_cases[p + f"vnd{k_max}_cost"]), p
+            np.testing.assert_array_equal(trace, small_cases[p + f"vnd{k_max}_trace"], err_msg=p)
+            np.testing.assert_array_equal(sm, small_cases[p + f"vnd{k_max}_sm"], err_msg=p)
+            np.testing.assert_array_equal(sr, small_cases[p + f"vnd{k_max}_sr"], err_msg=p)
+            _, _, _, _, ost = oracle.vnd(inst, small_cases[p + "sm"], small_cases[p + "sr"], k_max)
+            assert st["evals_reference"] == ost["evals"], p
+            assert st["moves"] == ost["moves"] and st["sweeps"] == ost["sweeps"], p
+
+
+def test_initial_solution_golden(small_cases):
+    for inst, dev, p in _cases(small_cases):
+        if p.endswith("_0_"):
+            sm, sr = dev.initial_solution()
+            np.testing.assert_array_equal(sm, small_cases[p + "sm"])
+            np.testing.assert_array_equal(sr, small_cases[p + "sr"])
+
+
+def test_decode_matches_oracle(small_cases):
+    for inst, dev, p in _cases(small_cases):
+        got = dev.decode(small_cases[p + "sm"], small_cases[p + "sr"])
+        want = oracle.decode(inst, small_cases[p + "sm"], small_cases[p + "sr"])
+        for g, w in zip(got, want):
+            np.testing.assert_array_equal(g, w, err_msg=p)
+
+
+def test_c1_every_lockstep_pass():
+    """BASELINE config 1 (K=10, T=52, seed 0): all 180 passes of the
+    reference trajectory, then the fused VND: cost 44,066,661."""
+    g = golden("c1_trajectory.npz")
+    inst = generate_instance(GeneratorConfig(products=10, periods=52, seed=0))
+    dev = DeviceInstance(inst)
+    sm, sr = g["start_sm"].copy(), g["start_sr"].copy()
+    for i in range(g["pass_dec"].shape[0]):
+        out, _ = dev.scan_products(sm, sr, i % 4 + 1)
+        dec = out[0]
+        for name, got in zip(NAMES, out):
+            got = np.array(got)
+            if name in ("m0", "r0"):
+                got &= dec > 0
+            if name in ("m1", "r1"):
+                got &= (dec > 0) & (out[4] >= 0)
+            np.testing.assert_array_equal(got, g["pass_" + name][i], err_msg=f"pass {i} {name}")
+        sm, sr = sm.copy(), sr.copy()
+        dev.apply_scan(out, sm, sr)
+    np.testing.assert_array_equal(sm, g["final_sm"])
+    fm, fr, trace, st = dev.vnd(g["start_sm"], g["start_sr"])
+    assert st["cost"] == int(g["cost"]) == 44066661
+    np.testing.assert_array_equal(trace, g["trace"])
+    np.testing.assert_array_equal(fm, g["final_sm"])
+    np.testing.assert_array_equal(fr, g["final_sr"])
+    assert st["evals_reference"] == int(g["evals"]) == 70890
+    assert st["moves"] == int(g["moves"]) == 738
+    assert st["sweeps"] == int(g["sweeps"]) == 45
+
+
+def test_k1000_vnd_golden():
+    g = golden("k1000.npz")
+    inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+    start = initial_solution(inst)
+    np.testing.assert_array_equal(np.packbits(start.setup_m, axis=1), g["start_sm"])
+    sm, sr, trace, st = DeviceInstance(inst).vnd(start.setup_m, start.setup_r)
+    assert st["cost"] == int(g["cost"]) == 4484593955
+    np.testing.assert_array_equal(trace, g["trace"])
+    np.testing.assert_array_equal(np.packbits(sm, axis=1), g["final_sm"])
+    np.testing.assert_array_equal(np.packbits(sr, axis=1), g["final_sr"])
+    assert st["evals_reference"] == int(g["evals"]) == 7814870
+    assert st["moves"] == int(g["moves"]) and st["sweeps"] == int(g["sweeps"])
+
+
+def _big():
+    with open(os.path.join(GOLDEN, "big.json")) as f:
+        return json.load(f)
+
+
+def test_c3_k100000_vnd_golden():
+    """BASELINE config 3 at full size: K=100,000, T=52 -- final cost
+    449,100,704,810, full trace and plan hash from the live reference."""
+    g = _big()["k100000_t52"]
+    inst = generate_instance(GeneratorConfig(products=100000, periods=52, seed=0))
+    start = initial_solution(inst)
+    assert _plan_sha(start.setup_m, start.setup_r) == g["start_plan_sha"]
+    sm, sr, trace, st = DeviceInstance(inst).vnd(start.setup_m, start.setup_r)
+    assert st["cost"] == g["cost"] == 449100704810
+    assert trace.tolist() == g["trace"]
+    assert _plan_sha(sm, sr) == g["plan_sha"]
+
+
+def test_c4_t520_sample_golden():
+    """BASELINE config 4 (T=520): products of the K=10,000 seed-0 instance;
+    per-product VND is exact by decomposition, so a sample pins the path."""
+    g = _big()["k10000_t520_sample"]
+    full = generate_instance(GeneratorConfig(products=10000, periods=520, seed=0))
+    sub = g["products"]
+    inst = Instance(len(sub), 520, full.demand[sub], full.returns[sub],
+                    full.setup_cost_m[sub], full.setup_cost_r[sub], full.holding_cost_m[sub],
+                    full.holding_cost_r[sub], full.unit_cost_m[sub], full.unit_cost_r[sub])
+    start = initial_solution(inst)
+    sm, sr, trace, st = DeviceInstance(inst).vnd(start.setup_m, start.setup_r)
+    assert st["cost"] == g["cost"]
+    assert trace.tolist() == g["trace"]
+    assert _plan_sha(sm, sr) == g["plan_sha"]
+
+
+def _random_instance(rng, K, T, big=False):
+    if big:   # force the int64 value / int64 cost paths
+        dem = rng.integers(0, 10**8, size=(K, T))
+        dem[rng.random((K, T)) < 0.3] = 0
+        ret = (rng.random((K, T)) * dem * rng.uniform(0, 1)).astype(np.int64)
+        c = [rng.integers(0, 10**9, size=K), rng.integers(0, 10**9, size=K),
+             rng.integers(0, 1000, size=K), rng.integers(0, 1000, size=K),
+             rng.integers(0, 1000, size=K), rng.integers(0, 1000, size=K)]
+    else:
+        dem = rng.integers(0, rng.integers(1, 120), size=(K, T))
+        dem[rng.random((K, T)) < rng.uniform(0, 0.6)] = 0
+        ret = (rng.random((K, T)) * dem * rng.uniform(0, 1.2)).astype(np.int64)
+        c = [rng.integers(0, 300_000, size=K), rng.integers(0, 300_000, size=K),
+             rng.integers(0, 600, size=K), rng.integers(0, 600, size=K),
+             rng.integers(0, 50, size=K), rng.integers(0, 50, size=K)]
+    return Instance(K, T, dem, ret, *c)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_against_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    T = int(rng.choice([1, 2, 3, 5, 8, 31, 32, 33, 52, 63, 64, 65, 100, 150]))
+    K = int(rng.integers(1, 60))
+    big = seed % 4 == 3
+    inst = _random_instance(rng, K, T, big)
+    dev = DeviceInstance(inst)
+    plans = [initial_solution(inst)]
+    plans.append(type(plans[0])(rng.random((K, T)) < 0.5, rng.random((K, T)) < 0.3))
+    plans.append(type(plans[0])(np.ones((K, T), bool), rng.random((K, T)) < 0.5))
+    for plan in plans:
+        np.testing.assert_array_equal(dev.product_costs(plan.setup_m, plan.setup_r),
+                                      oracle.product_costs(inst, plan.setup_m, plan.setup_r))
+        for nbh in (1, 2, 3, 4):
+            out, ev = dev.scan_products(plan.setup_m, plan.setup_r, nbh)
+            want, oev = oracle.scan_products(inst, plan.setup_m, plan.setup_r, nbh)
+            assert ev == oev
+            np.testing.assert_array_equal(out[0], want[0])
+            np.testing.assert_array_equal(out[1], want[1])
+            np.testing.assert_array_equal(out[4], want[4])
+            w = want[0] > 0
+            for i in (2, 3):
+                np.testing.assert_array_equal(out[i][w], want[i][w])
+        for k_max in (2, 4):
+            sm, sr, trace, st = dev.vnd(plan.setup_m, plan.setup_r, k_max)
+            om, orr, ocost, otrace, ost = oracle.vnd(inst, plan.setup_m, plan.setup_r, k_max)
+            assert st["cost"] == ocost
+            np.testing.assert_array_equal(trace, otrace)
+            np.testing.assert_array_equal(sm, om)
+            np.testing.assert_array_equal(sr, orr)
+            assert st["evals_reference"] == ost["evals"]
+
+
+def test_wide_int64_path():
+    """Values too large for int32 take the int64-value / int64-cost path."""
+    rng = np.random.default_rng(77)
+    K, T = 9, 40
+    dem = rng.integers(10**8, 10**9, size=(K, T))
+    dem[rng.random((K, T)) < 0.3] = 0
+    ret = (rng.random((K, T)) * dem * 0.7).astype(np.int64)
+    c = [rng.integers(0, 10**9, size=K), rng.integers(0, 10**9, size=K),
+         rng.integers(0, 1000, size=K), rng.integers(0, 1000, size=K),
+         rng.integers(0, 1000, size=K), rng.integers(0, 1000, size=K)]
+    inst = Instance(K, T, dem, ret, *c)
+    dev = DeviceInstance(inst)
+    assert dev.info["value_bytes"] == 8 and dev.info["cost_bytes"] == 8
+    start = initial_solution(inst)
+    sm, sr, trace, st = dev.vnd(start.setup_m, start.setup_r)
+    om, orr, ocost, otrace, ost = oracle.vnd(inst, start.setup_m, start.setup_r)
+    assert st["cost"] == ocost
+    np.testing.assert_array_equal(trace, otrace)
+    np.testing.assert_array_equal(sm, om)
+    np.testing.assert_array_equal(sr, orr)
+    assert st["evals_reference"] == ost["evals"]
+
+
+def test_out_of_range_instance_rejected():
+    inst = Instance(1, 3, [[2**62, 0, 1]], [[0, 0, 0]], [1], [1], [1], [1])
+    with pytest.raises(ValueError):
+        DeviceInstance(inst)
+
+
+def test_mixed_width_t520_paths():
+    """T=520-style instances take the int32-value / int64-cost path."""
+    inst = generate_instance(GeneratorConfig(products=6, periods=300, seed=3))
+    dev = DeviceInstance(inst)
+    assert dev.info["value_bytes"] == 4 and dev.info["cost_bytes"] == 8
+    start = initial_solution(inst)
+    sm, sr, trace, st = dev.vnd(start.setup_m, start.setup_r)
+    om, orr, ocost, otrace, _ = oracle.vnd(inst, start.setup_m, start.setup_r, threads=6)
+    assert st["cost"] == ocost
+    np.testing.assert_array_equal(trace, otrace)
+    np.testing.assert_array_equal(sm, om)
