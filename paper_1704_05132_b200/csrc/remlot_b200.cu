@@ -250,11 +250,17 @@ struct VndOut {
 // into trace_dec[sweep * k_max + nbh - 1] with exact int64 atomics so the
 // reference's lockstep trace is reproduced.  The next product's rows are
 // prefetched by TMA while the current one is processed.
-#ifndef RL_VND_MINB
-#define RL_VND_MINB 1
+// CTAs per SM the register allocation must allow (register-light int32 /
+// register-mask variant runs 6 x 4 warps per SM; measured).
+template <typename V, typename C, typename Mask> struct VndMinBlocks { static constexpr int value = 1; };
+template <> struct VndMinBlocks<int32_t, int32_t, MaskReg> { static constexpr int value = 6; };
+#ifdef RL_VND_MINB
+#define RL_VND_MINB_OF(V, C, M) RL_VND_MINB
+#else
+#define RL_VND_MINB_OF(V, C, M) VndMinBlocks<V, C, M>::value
 #endif
 template <typename V, typename C, typename Mask>
-__global__ void __launch_bounds__(128, RL_VND_MINB) k_vnd(InstView<V> in, const uint8_t *sm_in,
+__global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstView<V> in, const uint8_t *sm_in,
                                              const uint8_t *sr_in, uint8_t *sm_out,
                                              uint8_t *sr_out, int k_max, VndOut o)
 {

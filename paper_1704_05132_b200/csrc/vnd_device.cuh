@@ -194,7 +194,7 @@ struct MaskSmem {
 
 // The rows of a candidate move: base rows with periods a <= b rewritten.
 struct PatchedSmem {
-    const MaskSmem &base;
+    MaskSmem base;
     int a, b;
     bool ma, ra, mb, rb;
     __device__ bool m(int t) const { return t == a ? ma : t == b ? mb : base.m(t); }
@@ -245,6 +245,7 @@ struct MaskReg {
 struct PatchedReg {
     uint64_t M, R;
     int T;
+    PatchedReg() = default;
     __device__ PatchedReg(const MaskReg &base, int a, int b, bool ma, bool ra, bool mb, bool rb)
     {
         const uint64_t ba = 1ull << a, bb = 1ull << b, clr = ~(ba | bb);
@@ -259,6 +260,7 @@ struct PatchedReg {
 
 template <typename Mask> struct PatchOf;
 template <> struct PatchOf<MaskSmem> {
+    using type = PatchedSmem;
     __device__ static PatchedSmem make(const MaskSmem &b, int a, int bb, bool ma, bool ra,
                                        bool mb, bool rb)
     {
@@ -266,6 +268,7 @@ template <> struct PatchOf<MaskSmem> {
     }
 };
 template <> struct PatchOf<MaskReg> {
+    using type = PatchedReg;
     __device__ static PatchedReg make(const MaskReg &b, int a, int bb, bool ma, bool ra, bool mb,
                                       bool rb)
     {
@@ -576,9 +579,42 @@ struct PassResult {
     int n_moves;  // candidates scored (list_moves count)
 };
 
+// Per-lane state of one delta walk (score_move unrolled into steps).
+template <typename V, typename C, typename Mask>
+struct Walk {
+    typename PatchOf<Mask>::type nw;
+    int u, b, slot;
+    V X;
+    C acc;
+};
+
+template <typename V, typename C, typename Mask>
+__device__ inline typename PatchOf<Mask>::type patch_of(const Mask &mk, const MoveDesc &d, int &a,
+                                                        int &b)
+{
+    if (d.p1 < 0) {
+        a = b = d.p0;
+        return PatchOf<Mask>::make(mk, d.p0, d.p0, d.m0, d.r0, d.m0, d.r0);
+    }
+    if (d.p1 < d.p0) {
+        a = d.p1;
+        b = d.p0;
+        return PatchOf<Mask>::make(mk, d.p1, d.p0, d.m1, d.r1, d.m0, d.r0);
+    }
+    a = d.p0;
+    b = d.p1;
+    return PatchOf<Mask>::make(mk, d.p0, d.p1, d.m0, d.r0, d.m1, d.r1);
+}
+
 // One neighborhood pass over the warp's product (scan_products body,
 // _kernels.py:280-325): enumerate, score every move, keep the strict
 // minimum with the earliest slot on ties.  best_out = winning S.
+//
+// Moves are scored by delta walks of data-dependent length, so the lanes
+// run a warp-level work queue over walk *steps*: a lane whose walk ends
+// takes the next unscored move, and every loop iteration advances every
+// busy lane by one segment.  Each lane still scores its moves in
+// increasing slot order, so a strict '<' keeps the earliest on ties.
 template <typename V, typename C, typename Mask>
 __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int T,
                                        const ProductCosts<C> &pc, C S, int nbh, int lane,
@@ -603,14 +639,67 @@ __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int 
     }
     C best = S;
     int key = 0x7fffffff;
-    for (int i = lane; i < n; i += 32) {
-        const int slot = dense ? i : s.mv[i];
-        const MoveDesc d = slot_move(mk, nbh, slot, T);
-        C c;
-        if (score_desc(s, mk, d, T, pc, S, c) && c < best) {
-            best = c;
-            key = slot;
+    const unsigned lt = (1u << lane) - 1;
+    Walk<V, C, Mask> w;
+    int idx = lane, next = 32;
+    bool pend = idx < n, act = false;
+    while (__any_sync(FULL, pend | act)) {
+        if (pend) {
+            pend = false;
+            w.slot = dense ? idx : s.mv[idx];
+            const MoveDesc d = slot_move(mk, nbh, w.slot, T);
+            int a;
+            w.nw = patch_of<V, C, Mask>(mk, d, a, w.b);
+            w.u = mk.prev(a);
+            if (w.u < 0) {
+                w.u = w.nw.next(0);
+                w.acc = 0;
+                w.X = 0;
+                act = s.cd[w.u] == 0;   // demand before the first setup: infeasible
+            } else {
+                w.acc = s.cpre[w.u];
+                w.X = s.xin[w.u];
+                act = true;
+            }
+            if (act && w.u >= T) {   // no setup at all and no demand
+                act = false;
+                if (w.acc < best) {
+                    best = w.acc;
+                    key = w.slot;
+                }
+            }
         }
+        if (act) {
+            const int u = w.u, v = w.nw.next(u + 1);
+            C c;
+            V xr;
+            if (!seg_cost<V, C>(s.cd, s.cr, T, u, v, w.nw.m(u), w.nw.r(u), w.X, pc, c, xr)) {
+                act = false;
+            } else {
+                w.acc += c;
+                w.X += xr;
+                w.u = v;
+                bool done = v >= T;
+                if (!done && v > w.b && w.X == s.xin[v]) {
+                    w.acc += S - s.cpre[v];
+                    done = true;
+                }
+                if (done) {
+                    act = false;
+                    if (w.acc < best) {
+                        best = w.acc;
+                        key = w.slot;
+                    }
+                }
+            }
+        }
+        const bool idle = !(pend | act);
+        const unsigned m = __ballot_sync(FULL, idle);
+        if (idle) {
+            idx = next + __popc(m & lt);
+            pend = idx < n;
+        }
+        next += __popc(m);
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
