@@ -111,6 +111,29 @@ int rl_initial_solution_device(rl_instance *h, uint8_t *d_sm, uint8_t *d_sr, voi
 int rl_decode(rl_instance *h, const uint8_t *sm, const uint8_t *sr, int64_t *x_m,
               int64_t *x_r, int64_t *y_m, int64_t *y_r, int64_t *cost);
 
+/* ---- device GVNS (reference gvns.py:88-244) ----------------------------
+ * rl_gvns_begin uploads an incumbent plan (must be feasible), computes the
+ * lot-for-lot start and F = the VND image of the incumbent, sets strength 1.
+ * workers = W, k_max = shake strength bound, k_vnd_max in 1..4, seed = the
+ * solver seed (used mod 2^64 like gvns.py:89).  *inc_cost = evaluate(inc). */
+int rl_gvns_begin(rl_instance *h, int workers, int k_max, int k_vnd_max, uint64_t seed,
+                  const uint8_t *sm, const uint8_t *sr, int64_t *inc_cost);
+/* Overwrite the shake strength k (worker_round(..., k, ...)). */
+int rl_gvns_set_strength(rl_instance *h, int64_t strength);
+/* One round (worker_round, gvns.py:147-174) with round index round_index;
+ * accept = 1 also applies the GVNS step (gvns.py:207-215) on the device
+ * (accept strict improvement, next_strength).  Asynchronous. */
+int rl_gvns_round(rl_instance *h, int64_t round_index, int accept);
+/* which = 0: incumbent, 1: last round's winning candidate (accept = 0).
+ * info[0..5] = incumbent cost, strength, last best cost, last best worker,
+ * accepted rounds, shake fallbacks in the last round.  sm/sr may be NULL. */
+int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr, int64_t *info);
+/* Test hook: numpy-exact Philox stream of SeedSequence((seed, round,
+ * worker)) on the device: out = 4 raw next64, choice(pop, size,
+ * replace=False), shuffle of [1, 4, 7, ...] (shuffle_n), one more next64. */
+int rl_rng_probe(uint64_t seed, uint64_t round, uint64_t worker, int64_t pop, int64_t size,
+                 int64_t shuffle_n, int64_t *out);
+
 /* Measured INT32 throughput of the current device (integer ops/s; IMAD +
  * LOP3 chains over all SMs): the roofline denominator of the ALU-bound VND
  * kernel. */

@@ -22,7 +22,8 @@ RL_ERANGE = -4
 EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_instance_info", "rl_product_costs", "rl_scan_products", "rl_apply_scan",
            "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect",
-           "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_int_peak", "rl_launch_count",
+           "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
+           "rl_gvns_round", "rl_gvns_state", "rl_rng_probe", "rl_launch_count",
            "rl_last_error")
 
 _lib = None
@@ -61,6 +62,11 @@ def load():
         "rl_initial_solution_device": (I, [P, P, P, P]),
         "rl_decode": (I, [P] + [P] * 7),
         "rl_int_peak": (I, [P]),
+        "rl_gvns_begin": (I, [P, I, I, I, ctypes.c_uint64, P, P, P]),
+        "rl_gvns_set_strength": (I, [P, I64]),
+        "rl_gvns_round": (I, [P, I64, I]),
+        "rl_gvns_state": (I, [P, I, P, P, P]),
+        "rl_rng_probe": (I, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, I64, I64, I64, P]),
         "rl_launch_count": (I64, [P]),
         "rl_last_error": (ctypes.c_char_p, []),
     }
@@ -190,6 +196,34 @@ class DeviceInstance:
               "rl_decode")
         return outs[0], outs[1], outs[2], outs[3], cost
 
+    # ---- device GVNS (gvns_impl.cuh)
+    def gvns_begin(self, workers, k_max, k_vnd_max, seed, sm, sr):
+        sm, sr = u8(sm), u8(sr)
+        cost = np.zeros(1, np.int64)
+        check(load().rl_gvns_begin(self.h, workers, k_max, k_vnd_max, seed & ((1 << 64) - 1),
+                                   ptr(sm), ptr(sr), ptr(cost)), "rl_gvns_begin")
+        return int(cost[0])
+
+    def gvns_set_strength(self, k):
+        check(load().rl_gvns_set_strength(self.h, k), "rl_gvns_set_strength")
+
+    def gvns_round(self, round_index, accept):
+        check(load().rl_gvns_round(self.h, round_index, 1 if accept else 0), "rl_gvns_round")
+
+    def gvns_state(self, which, want_plan=True):
+        """which 0 = incumbent, 1 = last candidate -> (sm, sr, info dict)."""
+        info = np.zeros(6, np.int64)
+        sm = sr = None
+        if want_plan:
+            sm = np.empty((self.K, self.T), np.bool_)
+            sr = np.empty((self.K, self.T), np.bool_)
+        check(load().rl_gvns_state(self.h, which, ptr(sm.view(np.uint8)) if want_plan else None,
+                                   ptr(sr.view(np.uint8)) if want_plan else None, ptr(info)),
+              "rl_gvns_state")
+        return sm, sr, dict(inc_cost=int(info[0]), strength=int(info[1]),
+                            best_cost=int(info[2]), best_worker=int(info[3]),
+                            accepted=int(info[4]), fallbacks=int(info[5]))
+
     def initial_solution(self):
         sm = np.empty((self.K, self.T), np.bool_)
         sr = np.empty((self.K, self.T), np.bool_)
@@ -212,6 +246,15 @@ def list_moves(nbh, sm_row, sr_row):
     c = int(n[0])
     return (mp0[:c], b[0][:c].view(np.bool_), b[1][:c].view(np.bool_), mp1[:c],
             b[2][:c].view(np.bool_), b[3][:c].view(np.bool_))
+
+
+def rng_probe(seed, round_index, worker, pop, size, shuffle_n):
+    """Device Philox stream (test hook): raw[4], choice, shuffled, raw[1]."""
+    out = np.zeros(4 + size + shuffle_n + 1, np.int64)
+    check(load().rl_rng_probe(seed & ((1 << 64) - 1), round_index, worker, pop, size, shuffle_n,
+                              ptr(out)), "rl_rng_probe")
+    return (out[:4].view(np.uint64), out[4:4 + size], out[4 + size:4 + size + shuffle_n],
+            out[-1:].view(np.uint64))
 
 
 def device_instance(inst):

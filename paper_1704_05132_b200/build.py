@@ -1,5 +1,6 @@
 """Build libremlot_b200.so in-tree with nvcc for sm_100a (no JIT cache)."""
 
+import glob
 import os
 import subprocess
 import sys
@@ -7,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "remlot_b200.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "vnd_device.cuh"),
-        os.path.join(ROOT, "include", "remlot_b200.h")]
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu*"))) + [
+    os.path.join(ROOT, "include", "remlot_b200.h")]
 OUT = os.path.join(HERE, "_lib", "libremlot_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

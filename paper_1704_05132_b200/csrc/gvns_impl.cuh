@@ -1,0 +1,646 @@
+// gvns_impl.cuh -- device shaking, W-worker rounds and the best-of join
+// (reference gvns.py:88-221).  Included by remlot_b200.cu after the handle.
+//
+// A round (worker_round, gvns.py:147-174) runs W workers; worker w draws from
+// Philox(SeedSequence((seed, round, w))) exactly like numpy (rng_device.cuh),
+// flips k_eff = min(k, 2KT) distinct flat positions (gvns.py:93-122), and
+// descends with VND.  Because products never interact and the VND of a plan
+// is the per-product VND of its rows, a worker's
+// result is F (the per-product VND image of the incumbent, computed once)
+// with only its touched products re-descended.  So a round is:
+//   k_shake           thread per worker: draws, touched rows, feasibility
+//   k_shake_fallback  thread per worker whose 50 draws failed (gvns.py:124-137)
+//   k_gvns_vnd        warp per (worker, touched product) [+ fallback plans]
+//   k_gvns_join       block: min (cost, worker) join, accept, next strength
+// with no host synchronisation; the incumbent and F stay resident.
+
+struct GvnsArgs {
+    int64_t K, KT, pop;
+    int T, NW, W, k_max, kcap, tcap, tsize, fb_slots;
+    uint64_t seed;
+    uint8_t *inc, *F, *init, *cand;   // 2KT bytes each: m rows then r rows
+    int64_t *Fcost;                   // K
+    int64_t *scal;                    // see GV_* below
+    int64_t *pos;                     // W x kcap
+    uint64_t *table;                  // W x tsize
+    int64_t *tailidx;                 // W x pop (only when the tail shuffle is needed)
+    int64_t *tp;                      // W x tcap touched products
+    int *tn, *fb, *fbslot;            // W
+    uint32_t *tw;                     // W x tcap x 2 x NW
+    int64_t *tcost;                   // W x tcap
+    PhiloxState *rng;                 // W
+    uint8_t *fbplan;                  // fb_slots x 2KT
+    int64_t *fbdiff;                  // fb_slots x pop
+    int64_t *fbpcost;                 // fb_slots x K
+    int *queue;
+};
+
+enum {
+    GV_INC_COST = 0,
+    GV_FTOT,
+    GV_STRENGTH,
+    GV_INC_IS_F,
+    GV_BEST_COST,
+    GV_BEST_W,
+    GV_ACCEPTED,
+    GV_FB_COUNT,
+    GV_ERROR,
+    GV_FBCOST0,   // fb_slots entries follow
+};
+
+// Feasibility of one product's rows under row_cost (_kernels.py:58-82):
+// no demand before the first setup, and every segment whose demand exceeds
+// the remanufactured quantity has a manufacturing setup.
+template <typename V, typename BitM, typename BitR>
+__device__ inline bool row_feasible(const V *d, const V *r, int T, BitM bm, BitR br)
+{
+    int t = 0;
+    V rec = 0;
+    for (; t < T && !(bm(t) | br(t)); ++t) {
+        if (d[t] > 0)
+            return false;
+        rec += r[t];
+    }
+    while (t < T) {
+        const int u = t;
+        int v = u + 1;
+        V seg = d[u], ret = r[u];
+        while (v < T && !(bm(v) | br(v))) {
+            seg += d[v];
+            ret += r[v];
+            ++v;
+        }
+        const V avail = rec + r[u];
+        const V xr = br(u) ? (seg < avail ? seg : avail) : V(0);
+        if (seg - xr > 0 && !bm(u))
+            return false;
+        rec += ret - xr;
+        t = v;
+    }
+    return true;
+}
+
+template <typename V>
+__global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
+{
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= g.W)
+        return;
+    Philox rng;
+    rng.seed(g.seed, (uint64_t)round, (uint64_t)w);
+    const int64_t strength = g.scal[GV_STRENGTH];
+    const int64_t k_eff = strength < g.pop ? strength : g.pop;   // gvns.py:113
+    int64_t *P = g.pos + (int64_t)w * g.kcap;
+    int64_t *tp = g.tp + (int64_t)w * g.tcap;
+    uint32_t *tw = g.tw + (int64_t)w * g.tcap * 2 * g.NW;
+    const int T = g.T, NW = g.NW;
+    for (int attempt = 0; attempt < 50; ++attempt) {   // _SHAKE_REDRAWS (gvns.py:29, :114)
+        if (choice_uses_tail_shuffle(g.pop, k_eff))
+            choice_tail(rng, g.pop, k_eff, P, g.tailidx + (int64_t)w * g.pop);
+        else
+            choice_floyd(rng, g.pop, k_eff, P, g.table + (int64_t)w * g.tsize);
+        int n = 0;
+        for (int64_t i = 0; i < k_eff; ++i) {   // _flip_flat (gvns.py:93-98)
+            const int64_t p = P[i];
+            const int mat = p < g.KT ? 0 : 1;
+            const int64_t rem = p % g.KT, k = rem / T;
+            const int t = (int)(rem % T);
+            int j = 0;
+            while (j < n && tp[j] != k)
+                ++j;
+            if (j == n) {
+                tp[n++] = k;
+                uint32_t *row = tw + (int64_t)j * 2 * NW;
+                for (int q = 0; q < 2 * NW; ++q)
+                    row[q] = 0;
+                const uint8_t *im = g.inc + k * T, *ir = g.inc + g.KT + k * T;
+                for (int q = 0; q < T; ++q) {
+                    row[q >> 5] |= (uint32_t)im[q] << (q & 31);
+                    row[NW + (q >> 5)] |= (uint32_t)ir[q] << (q & 31);
+                }
+            }
+            tw[(int64_t)j * 2 * NW + mat * NW + (t >> 5)] ^= 1u << (t & 31);
+        }
+        bool ok = true;
+        for (int j = 0; j < n && ok; ++j) {
+            const uint32_t *row = tw + (int64_t)j * 2 * NW;
+            const int64_t k = tp[j];
+            ok = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
+                                 [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
+                                 [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
+        }
+        if (ok) {
+            g.tn[w] = n;
+            g.fb[w] = 0;
+            return;
+        }
+    }
+    g.tn[w] = 0;
+    g.fb[w] = 1;
+    g.rng[w] = rng.st;
+}
+
+// gvns.py:124-137: flip the positions where the incumbent differs from the
+// lot-for-lot start, in rng.shuffle order, until >= k_eff flips and the whole
+// plan is feasible; else return the start.  One thread per failing worker
+// (rare: all 50 independent redraws must have failed).
+template <typename V>
+__global__ void k_shake_fallback(InstView<V> in, GvnsArgs g)
+{
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= g.W || !g.fb[w])
+        return;
+    const int slot = atomicAdd((unsigned long long *)&g.scal[GV_FB_COUNT], 1ull);
+    if (slot >= g.fb_slots) {
+        atomicExch((unsigned long long *)&g.scal[GV_ERROR], 1ull);
+        return;
+    }
+    g.fbslot[w] = slot;
+    const int T = g.T;
+    const int64_t KT = g.KT, K = g.K;
+    uint8_t *plan = g.fbplan + (int64_t)slot * 2 * KT;
+    int64_t *diff = g.fbdiff + (int64_t)slot * g.pop;
+    int64_t *bad = g.fbpcost + (int64_t)slot * K;   // infeasibility flags, then costs
+    for (int64_t i = 0; i < 2 * KT; ++i)
+        plan[i] = g.inc[i];
+    int64_t n = 0;
+    for (int64_t p = 0; p < KT; ++p)
+        if (g.inc[p] != g.init[p])
+            diff[n++] = p;
+    for (int64_t p = 0; p < KT; ++p)
+        if (g.inc[KT + p] != g.init[KT + p])
+            diff[n++] = p + KT;
+    Philox rng;
+    rng.st = g.rng[w];
+    rng.shuffle(diff, n);
+    const int64_t strength = g.scal[GV_STRENGTH];
+    const int64_t k_eff = strength < g.pop ? strength : g.pop;
+    for (int64_t k = 0; k < K; ++k)
+        bad[k] = 0;   // the incumbent is feasible
+    int64_t nbad = 0;
+    bool done = false;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t p = diff[i];
+        plan[p] ^= 1;
+        const int64_t k = (p % KT) / T;
+        const uint8_t *pm = plan + k * T, *pr = plan + KT + k * T;
+        const bool f = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
+                                       [&](int q) { return pm[q] != 0; },
+                                       [&](int q) { return pr[q] != 0; });
+        nbad += (f ? 0 : 1) - bad[k];
+        bad[k] = f ? 0 : 1;
+        if (i + 1 >= k_eff && nbad == 0) {
+            done = true;
+            break;
+        }
+    }
+    if (!done)
+        for (int64_t i = 0; i < 2 * KT; ++i)
+            plan[i] = g.init[i];
+}
+
+// VND of every (worker, touched product) task and of every product of the
+// fallback plans; warps pull tasks from a queue.
+template <typename V, typename C, typename Mask>
+__global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, int k_vnd_max)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = in.T, NW = g.NW;
+    Slot<V, C> s = carve<V, C>(smem + warp * slot_bytes<V, C>(T), T);
+    if (lane == 0)
+        mbar_init(s.bar);
+    __syncwarp();
+    uint32_t phase = 0;
+    const int64_t n_norm = (int64_t)g.W * g.tcap;
+    int64_t nfb = g.scal[GV_FB_COUNT];
+    nfb = nfb < g.fb_slots ? nfb : g.fb_slots;
+    const int64_t n_tasks = n_norm + nfb * g.K;
+    for (;;) {
+        int64_t task = 0;
+        if (lane == 0)
+            task = atomicAdd(g.queue, 1);
+        task = __shfl_sync(FULL, task, 0);
+        if (task >= n_tasks)
+            break;
+        int64_t k;
+        uint32_t *row = nullptr;
+        uint8_t *plan = nullptr;
+        int w = -1, j = -1, slot = -1;
+        if (task < n_norm) {
+            w = (int)(task / g.tcap);
+            j = (int)(task % g.tcap);
+            if (g.fb[w] || j >= g.tn[w])
+                continue;
+            k = g.tp[(int64_t)w * g.tcap + j];
+            row = g.tw + ((int64_t)w * g.tcap + j) * 2 * NW;
+        } else {
+            slot = (int)((task - n_norm) / g.K);
+            k = (task - n_norm) % g.K;
+            plan = g.fbplan + (int64_t)slot * 2 * g.KT;
+        }
+        stage_begin(s, in, k, lane);
+        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k);
+        Mask mk;
+        if (row) {
+            // words -> plan bytes layout for load_rows: go through the slot's mv buffer
+            uint8_t *tmp = (uint8_t *)s.mv;   // 2T+2 uint16 = 4T+4 bytes >= 2T
+            for (int t = lane; t < T; t += 32) {
+                tmp[t] = (row[t >> 5] >> (t & 31)) & 1u;
+                tmp[T + t] = (row[NW + (t >> 5)] >> (t & 31)) & 1u;
+            }
+            __syncwarp();
+            mk = load_rows(s, Mask{}, tmp, tmp + T, 0, T, lane);
+        } else {
+            mk = load_rows(s, Mask{}, plan, plan + g.KT, k, T, lane);
+        }
+        stage_end(s, in, k, lane, phase);
+        const C K0 = build_prefix(s, T, pc, lane);
+        C S0, S;
+        VndStats st;
+        vnd_product(s, mk, T, pc, k_vnd_max, lane, S0, S, st, nullptr, 0, nullptr);
+        const int64_t cost = (int64_t)(K0 + S);
+        if (row) {
+            __syncwarp();
+            for (int q = lane; q < 2 * NW; q += 32)
+                row[q] = 0;
+            __syncwarp();
+            for (int t = lane; t < T; t += 32) {
+                if (mk.m(t))
+                    atomicOr(&row[t >> 5], 1u << (t & 31));
+                if (mk.r(t))
+                    atomicOr(&row[NW + (t >> 5)], 1u << (t & 31));
+            }
+            if (lane == 0)
+                g.tcost[(int64_t)w * g.tcap + j] = cost;
+        } else {
+            store_rows(mk, plan, plan + g.KT, k, T, lane);
+            if (lane == 0) {
+                g.fbpcost[(int64_t)slot * g.K + k] = cost;
+                atomicAdd((unsigned long long *)&g.scal[GV_FBCOST0 + slot], (unsigned long long)cost);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Join (gvns.py:170-174: min cost, lowest worker on ties) and, in accept
+// mode, the GVNS step (gvns.py:207-215): accept strict improvements, reset or
+// advance the strength (next_strength, gvns.py:177-181).  mode 0 writes the
+// winning candidate plan to g.cand (worker_round's return value).
+__global__ void k_gvns_join(GvnsArgs g, int mode)
+{
+    __shared__ long long s_cost[32];
+    __shared__ int s_w[32];
+    __shared__ int s_accept;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    long long best = 0x7fffffffffffffffll;
+    int bw = 0x7fffffff;
+    for (int w = tid; w < g.W; w += blockDim.x) {
+        long long c;
+        if (g.fb[w]) {
+            const int slot = g.fbslot[w];
+            c = slot < g.fb_slots ? g.scal[GV_FBCOST0 + slot] : 0x7fffffffffffffffll;
+        } else {
+            c = g.scal[GV_FTOT];
+            for (int j = 0; j < g.tn[w]; ++j) {
+                c -= g.Fcost[g.tp[(int64_t)w * g.tcap + j]];
+                c += g.tcost[(int64_t)w * g.tcap + j];
+            }
+        }
+        if (c < best || (c == best && w < bw)) {
+            best = c;
+            bw = w;
+        }
+    }
+    for (int off = 16; off; off >>= 1) {
+        const long long oc = __shfl_xor_sync(FULL, best, off);
+        const int ow = __shfl_xor_sync(FULL, bw, off);
+        if (oc < best || (oc == best && ow < bw)) {
+            best = oc;
+            bw = ow;
+        }
+    }
+    if (lane == 0) {
+        s_cost[wid] = best;
+        s_w[wid] = bw;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+            if (s_cost[i] < s_cost[0] || (s_cost[i] == s_cost[0] && s_w[i] < s_w[0])) {
+                s_cost[0] = s_cost[i];
+                s_w[0] = s_w[i];
+            }
+        g.scal[GV_BEST_COST] = s_cost[0];
+        g.scal[GV_BEST_W] = s_w[0];
+        int acc = 0;
+        if (mode == 1) {
+            acc = s_cost[0] < g.scal[GV_INC_COST];
+            const int64_t k = g.scal[GV_STRENGTH];
+            g.scal[GV_STRENGTH] = (acc || k >= g.k_max) ? 1 : k + 1;
+        }
+        s_accept = mode == 0 ? 1 : acc;
+    }
+    __syncthreads();
+    const int w = s_w[0];
+    if (!s_accept)
+        return;
+    // the candidate: F with the winner's touched rows, or its fallback plan
+    uint8_t *dst = mode == 0 ? g.cand : g.inc;
+    const int64_t KT2 = 2 * g.KT;
+    if (g.fb[w]) {
+        const uint8_t *src = g.fbplan + (int64_t)g.fbslot[w] * KT2;
+        for (int64_t i = tid; i < KT2; i += blockDim.x) {
+            dst[i] = src[i];
+            if (mode == 1)
+                g.F[i] = src[i];
+        }
+        if (mode == 1)
+            for (int64_t k = tid; k < g.K; k += blockDim.x)
+                g.Fcost[k] = g.fbpcost[(int64_t)g.fbslot[w] * g.K + k];
+    } else {
+        if (mode == 0 || !g.scal[GV_INC_IS_F])
+            for (int64_t i = tid; i < KT2; i += blockDim.x)
+                dst[i] = g.F[i];
+        __syncthreads();
+        const int NW = g.NW, T = g.T;
+        const int n = g.tn[w];
+        for (int64_t q = tid; q < (int64_t)n * T; q += blockDim.x) {
+            const int j = (int)(q / T), t = (int)(q % T);
+            const int64_t k = g.tp[(int64_t)w * g.tcap + j];
+            const uint32_t *row = g.tw + ((int64_t)w * g.tcap + j) * 2 * NW;
+            const uint8_t bm = (row[t >> 5] >> (t & 31)) & 1u, br = (row[NW + (t >> 5)] >> (t & 31)) & 1u;
+            dst[k * T + t] = bm;
+            dst[g.KT + k * T + t] = br;
+            if (mode == 1) {
+                g.F[k * T + t] = bm;
+                g.F[g.KT + k * T + t] = br;
+            }
+        }
+        if (mode == 1 && tid < n)
+            g.Fcost[g.tp[(int64_t)w * g.tcap + tid]] = g.tcost[(int64_t)w * g.tcap + tid];
+    }
+    __syncthreads();
+    if (mode == 1 && tid == 0) {
+        g.scal[GV_INC_COST] = s_cost[0];
+        g.scal[GV_FTOT] = s_cost[0];
+        g.scal[GV_INC_IS_F] = 1;
+        g.scal[GV_ACCEPTED] += 1;
+    }
+}
+
+// ------------------------------------------------------------------ host
+
+struct GvnsState {
+    GvnsArgs a{};
+    int k_vnd_max = 4;
+    size_t tail_bytes = 0;
+    void *blocks[16] = {};
+    int nblocks = 0;
+};
+
+static void gvns_free(GvnsState *gs)
+{
+    if (!gs)
+        return;
+    for (int i = 0; i < gs->nblocks; ++i)
+        if (gs->blocks[i])
+            cudaFree(gs->blocks[i]);
+    delete gs;
+}
+
+template <typename P>
+static cudaError_t gv_alloc(GvnsState *gs, P **p, size_t bytes)
+{
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, bytes > 0 ? bytes : 8);
+    if (e == cudaSuccess) {
+        gs->blocks[gs->nblocks++] = q;
+        *p = (P *)q;
+    }
+    return e;
+}
+
+template <typename V, typename C, typename Mask>
+static int gv_launch_vnd(rl_instance *h, GvnsState *gs)
+{
+    int grid;
+    size_t smem;
+    int rc = launch_cfg<V, C>(h, (const void *)k_gvns_vnd<V, C, Mask>,
+                              (int64_t)gs->a.W * gs->a.tcap + (int64_t)gs->a.fb_slots * h->K,
+                              grid, smem);
+    if (rc)
+        return rc;
+    CK(cudaMemsetAsync(gs->a.queue, 0, sizeof(int), h->stream));
+    k_gvns_vnd<V, C, Mask><<<grid, kWarpsPerCta * 32, smem, h->stream>>>(view<V>(h), gs->a,
+                                                                          gs->k_vnd_max);
+    CKL();
+    return 0;
+}
+
+template <typename V, typename C>
+static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round)
+{
+    const int W = gs->a.W;
+    CK(cudaMemsetAsync(&gs->a.scal[GV_FB_COUNT], 0, 2 * sizeof(int64_t), h->stream));
+    CK(cudaMemsetAsync(&gs->a.scal[GV_FBCOST0], 0, gs->a.fb_slots * sizeof(int64_t), h->stream));
+    k_shake<V><<<(W + 63) / 64, 64, 0, h->stream>>>(view<V>(h), gs->a, round);
+    CKL();
+    k_shake_fallback<V><<<(W + 63) / 64, 64, 0, h->stream>>>(view<V>(h), gs->a);
+    CKL();
+    return 0;
+}
+
+extern "C" int rl_gvns_begin(rl_instance *h, int workers, int k_max, int k_vnd_max,
+                             uint64_t seed, const uint8_t *sm, const uint8_t *sr,
+                             int64_t *inc_cost)
+{
+    (void)cudaGetLastError();
+    if (!h || !sm || !sr || workers < 1 || k_max < 1 || k_vnd_max < 1 || k_vnd_max > 4)
+        return fail(RL_EINVAL, "rl_gvns_begin: bad arguments (workers=%d k_max=%d k_vnd_max=%d)",
+                    workers, k_max, k_vnd_max);
+    CK(cudaSetDevice(h->device));
+    const int64_t K = h->K, KT = K * h->T, pop = 2 * KT;
+    const int T = h->T, NW = (T + 31) / 32;
+    const int64_t keff_max = k_max < pop ? k_max : pop;
+    GvnsState *gs = h->gv;
+    const bool reuse = gs && gs->a.W == workers && gs->a.k_max == k_max;
+    if (!reuse) {
+        gvns_free(gs);
+        h->gv = gs = new GvnsState();
+        GvnsArgs &a = gs->a;
+        a.K = K;
+        a.KT = KT;
+        a.pop = pop;
+        a.T = T;
+        a.NW = NW;
+        a.W = workers;
+        a.k_max = k_max;
+        a.kcap = (int)keff_max;
+        a.tcap = (int)(keff_max < K ? keff_max : K);
+        a.tsize = (int)(choice_table_mask(keff_max) + 1);
+        const double per_slot = (double)pop * (1 + 8) + 8.0 * K;
+        int fbs = (int)(512.0 * (1 << 20) / per_slot);
+        fbs = fbs < 1 ? 1 : fbs;
+        fbs = fbs > workers ? workers : fbs;
+        a.fb_slots = fbs > 64 && workers > 64 ? 64 : fbs;
+        cudaError_t e = gv_alloc(gs, &a.inc, 4 * (size_t)pop);
+        if (e == cudaSuccess) {
+            a.F = a.inc + pop;
+            a.init = a.F + pop;
+            a.cand = a.init + pop;
+            e = gv_alloc(gs, &a.Fcost, K * 8);
+        }
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.scal, (GV_FBCOST0 + a.fb_slots) * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.pos, (size_t)workers * a.kcap * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.table, (size_t)workers * a.tsize * 8);
+        if (e == cudaSuccess && choice_uses_tail_shuffle(pop, keff_max))
+            e = gv_alloc(gs, &a.tailidx, (size_t)workers * pop * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.tp, (size_t)workers * a.tcap * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.tn, (size_t)workers * 3 * sizeof(int));
+        if (e == cudaSuccess) {
+            a.fb = a.tn + workers;
+            a.fbslot = a.fb + workers;
+            e = gv_alloc(gs, &a.tw, (size_t)workers * a.tcap * 2 * NW * 4);
+        }
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.tcost, (size_t)workers * a.tcap * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.rng, (size_t)workers * sizeof(PhiloxState));
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.fbplan, (size_t)a.fb_slots * pop);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.fbdiff, (size_t)a.fb_slots * pop * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.fbpcost, (size_t)a.fb_slots * K * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.queue, 16);
+        if (e != cudaSuccess) {
+            gvns_free(gs);
+            h->gv = nullptr;
+            return fail(RL_ECUDA, "rl_gvns_begin: %s", cudaGetErrorString(e));
+        }
+    }
+    GvnsArgs &a = gs->a;
+    a.seed = seed;
+    gs->k_vnd_max = k_vnd_max;
+    // incumbent, lot-for-lot start, and F = per-product VND image of the incumbent
+    CK(cudaMemcpyAsync(a.inc, sm, KT, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(a.inc + KT, sr, KT, cudaMemcpyHostToDevice, h->stream));
+    int rc = rl_initial_solution_device(h, a.init, a.init + KT, h->stream);
+    if (rc)
+        return rc;
+    rc = rl_vnd_device(h, k_vnd_max, a.inc, a.inc + KT, a.F, a.F + KT, h->stream);
+    if (rc)
+        return rc;
+    CK(cudaMemcpyAsync(a.Fcost, h->p64 + K, K * 8, cudaMemcpyDeviceToDevice, h->stream));
+    int64_t sum[16];
+    CK(cudaMemcpyAsync(sum, h->summary, sizeof sum, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (sum[1] == RL_INFEASIBLE)
+        return fail(RL_EINVAL, "rl_gvns_begin: the incumbent plan is infeasible");
+    int64_t scal[GV_FBCOST0] = {};
+    scal[GV_INC_COST] = sum[1];
+    scal[GV_FTOT] = sum[0];
+    scal[GV_STRENGTH] = 1;
+    scal[GV_INC_IS_F] = 0;
+    CK(cudaMemcpyAsync(a.scal, scal, sizeof scal, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (inc_cost)
+        *inc_cost = sum[1];
+    return 0;
+}
+
+extern "C" int rl_gvns_set_strength(rl_instance *h, int64_t strength)
+{
+    (void)cudaGetLastError();
+    if (!h || !h->gv || strength < 1)
+        return fail(RL_EINVAL, "rl_gvns_set_strength: bad arguments");
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpyAsync(&h->gv->a.scal[GV_STRENGTH], &strength, 8, cudaMemcpyHostToDevice,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return 0;
+}
+
+extern "C" int rl_gvns_round(rl_instance *h, int64_t round_index, int accept)
+{
+    (void)cudaGetLastError();
+    if (!h || !h->gv || round_index < 0)
+        return fail(RL_EINVAL, "rl_gvns_round: call rl_gvns_begin first");
+    CK(cudaSetDevice(h->device));
+    GvnsState *gs = h->gv;
+    int rc = RL_DISPATCH(h, gv_launch_shake, h, gs, round_index);
+    if (rc)
+        return rc;
+    if ((rc = RL_DISPATCH_M(h, gv_launch_vnd, h, gs)))
+        return rc;
+    k_gvns_join<<<1, 1024, 0, h->stream>>>(gs->a, accept ? 1 : 0);
+    CKL();
+    return 0;
+}
+
+extern "C" int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr, int64_t *info)
+{
+    (void)cudaGetLastError();
+    if (!h || !h->gv || !info)
+        return fail(RL_EINVAL, "rl_gvns_state: bad arguments");
+    CK(cudaSetDevice(h->device));
+    GvnsArgs &a = h->gv->a;
+    int64_t scal[GV_FBCOST0];
+    CK(cudaMemcpyAsync(scal, a.scal, sizeof scal, cudaMemcpyDeviceToHost, h->stream));
+    const uint8_t *src = which == 0 ? a.inc : a.cand;
+    if (sm)
+        CK(cudaMemcpyAsync(sm, src, a.KT, cudaMemcpyDeviceToHost, h->stream));
+    if (sr)
+        CK(cudaMemcpyAsync(sr, src + a.KT, a.KT, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (scal[GV_ERROR])
+        return fail(RL_ECUDA, "gvns: more shake fallbacks in one round than slots (%d)",
+                    a.fb_slots);
+    info[0] = scal[GV_INC_COST];
+    info[1] = scal[GV_STRENGTH];
+    info[2] = scal[GV_BEST_COST];
+    info[3] = scal[GV_BEST_W];
+    info[4] = scal[GV_ACCEPTED];
+    info[5] = scal[GV_FB_COUNT];
+    return 0;
+}
+
+// Test hook: the numpy-exact RNG on the device (raw draws, choice, shuffle).
+__global__ void k_rng_probe(uint64_t seed, uint64_t round, uint64_t worker, int64_t pop,
+                            int64_t size, int64_t shuffle_n, int64_t *out, uint64_t *table,
+                            int64_t *idx)
+{
+    Philox g;
+    g.seed(seed, round, worker);
+    for (int i = 0; i < 4; ++i)
+        out[i] = (int64_t)g.next64();
+    if (choice_uses_tail_shuffle(pop, size))
+        choice_tail(g, pop, size, out + 4, idx);
+    else
+        choice_floyd(g, pop, size, out + 4, table);
+    int64_t *sh = out + 4 + size;
+    for (int64_t i = 0; i < shuffle_n; ++i)
+        sh[i] = 3 * i + 1;
+    g.shuffle(sh, shuffle_n);
+    out[4 + size + shuffle_n] = (int64_t)g.next64();
+}
+
+extern "C" int rl_rng_probe(uint64_t seed, uint64_t round, uint64_t worker, int64_t pop,
+                            int64_t size, int64_t shuffle_n, int64_t *out)
+{
+    (void)cudaGetLastError();
+    if (!out || pop < 1 || size < 0 || size > pop || shuffle_n < 0 || size > (1 << 20) ||
+        shuffle_n > (1 << 20) || (choice_uses_tail_shuffle(pop, size) && pop > ((int64_t)1 << 26)))
+        return fail(RL_EINVAL, "rl_rng_probe: bad arguments");
+    const int64_t n_out = 4 + size + shuffle_n + 1;
+    const uint64_t tsize = choice_table_mask(size) + 1;
+    const bool tail = choice_uses_tail_shuffle(pop, size);
+    int64_t *d;
+    CK(cudaMalloc(&d, (n_out + tsize + (tail ? pop : 1)) * 8));
+    k_rng_probe<<<1, 1>>>(seed, round, worker, pop, size, shuffle_n, d, (uint64_t *)(d + n_out),
+                          d + n_out + tsize);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpy(out, d, n_out * 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess)
+        return fail(RL_ECUDA, "rl_rng_probe: %s", cudaGetErrorString(e));
+    return 0;
+}

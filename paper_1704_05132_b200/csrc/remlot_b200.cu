@@ -19,6 +19,7 @@
 #include <string>
 
 #include "../../include/remlot_b200.h"
+#include "rng_device.cuh"
 #include "vnd_device.cuh"
 
 using namespace rl;
@@ -235,6 +236,68 @@ __global__ void __launch_bounds__(128) k_scan(InstView<V> in, const uint8_t *sm,
         atomicAdd(evals, my_evals);
 }
 
+struct VndStats {
+    int64_t evals;
+    int sweeps, moves, ntot;
+};
+
+// One product's VND to its fixpoint (vnd.py:277-288 restricted to one
+// product): sweeps of N1..Nk_max, each pass scans and applies the best
+// strictly improving move.  S0/S = segment-cost sums before/after; pass
+// decreases go to trace_dec[sweep*k_max + nbh-1] when trace_dec != nullptr.
+// Returns the base plan's feasibility (an infeasible product is skipped,
+// _kernels.py:289-290, and counts one sweep).
+template <typename V, typename C, typename Mask>
+__device__ inline bool vnd_product(const Slot<V, C> &s, Mask &mk, int T, const ProductCosts<C> &pc,
+                                   int k_max, int lane, C &S0, C &S, VndStats &st,
+                                   unsigned long long *trace_dec, int64_t cap_sweeps,
+                                   int *overflow)
+{
+    st.evals = 0;
+    st.sweeps = 0;
+    st.moves = 0;
+    st.ntot = 0;
+    const bool feas = base_pass(s, mk, T, pc, lane, S);
+    S0 = S;
+    if (!feas) {
+        st.sweeps = 1;
+        return false;
+    }
+    bool dirty = false;
+    for (;;) {
+        bool improved = false;
+        for (int nbh = 1; nbh <= k_max; ++nbh) {
+            if (dirty) {
+                base_pass(s, mk, T, pc, lane, S);
+                dirty = false;
+            }
+            C best;
+            const PassResult r = scan_pass(s, mk, T, pc, S, nbh, lane, best);
+            st.evals += r.n_moves;
+            if (r.improved) {
+                apply_slot(mk, nbh, r.slot, T, lane);
+                dirty = true;
+                improved = true;
+                ++st.moves;
+                if (trace_dec && lane == 0) {
+                    if (st.sweeps < cap_sweeps)
+                        atomicAdd(&trace_dec[(int64_t)st.sweeps * k_max + nbh - 1],
+                                  (unsigned long long)(int64_t)(S - best));
+                    else
+                        atomicExch(overflow, 1);
+                }
+                S = best;
+            }
+        }
+        ++st.sweeps;
+        if (!improved)
+            break;
+    }
+    for (int nbh = 1; nbh <= k_max; ++nbh)
+        st.ntot += move_count(mk, nbh, T, lane);
+    return true;
+}
+
 struct VndOut {
     int64_t *start_cost, *final_cost, *evals, *ntot;
     int32_t *sweeps, *moves;
@@ -292,55 +355,18 @@ __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstVie
         if (next < in.K)
             stage_begin(s, in, next, lane);
 
-        C S;
-        const bool feas = base_pass(s, mk, T, pc, lane, S);
-        int64_t evals = 0;
-        int sweeps = 0, moves = 0, ntot = 0;
-        const C S0 = S;
-        if (feas) {
-            bool dirty = false;
-            for (;;) {
-                bool improved = false;
-                for (int nbh = 1; nbh <= k_max; ++nbh) {
-                    if (dirty) {
-                        base_pass(s, mk, T, pc, lane, S);
-                        dirty = false;
-                    }
-                    C best;
-                    const PassResult r = scan_pass(s, mk, T, pc, S, nbh, lane, best);
-                    evals += r.n_moves;
-                    if (r.improved) {
-                        apply_slot(mk, nbh, r.slot, T, lane);
-                        dirty = true;
-                        improved = true;
-                        ++moves;
-                        if (lane == 0) {
-                            if (sweeps < o.cap_sweeps)
-                                atomicAdd(&o.trace_dec[(int64_t)sweeps * k_max + nbh - 1],
-                                          (unsigned long long)(int64_t)(S - best));
-                            else
-                                atomicExch(o.overflow, 1);
-                        }
-                        S = best;
-                    }
-                }
-                ++sweeps;
-                if (!improved)
-                    break;
-            }
-            for (int nbh = 1; nbh <= k_max; ++nbh)
-                ntot += move_count(mk, nbh, T, lane);
-        } else {
-            sweeps = 1;
-        }
+        C S, S0;
+        VndStats st;
+        const bool feas = vnd_product(s, mk, T, pc, k_max, lane, S0, S, st, o.trace_dec,
+                                      o.cap_sweeps, o.overflow);
         store_rows(mk, sm_out, sr_out, k, T, lane);
         if (lane == 0) {
             o.start_cost[k] = feas ? (int64_t)(K0 + S0) : RL_INFEASIBLE;
             o.final_cost[k] = feas ? (int64_t)(K0 + S) : RL_INFEASIBLE;
-            o.evals[k] = evals;
-            o.ntot[k] = ntot;
-            o.sweeps[k] = sweeps;
-            o.moves[k] = moves;
+            o.evals[k] = st.evals;
+            o.ntot[k] = st.ntot;
+            o.sweeps[k] = st.sweeps;
+            o.moves[k] = st.moves;
         }
         __syncwarp();
         k = next;
@@ -564,7 +590,11 @@ struct rl_instance {
     int last_kmax = 4;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timing = false;
+    struct GvnsState *gv = nullptr;        // device GVNS state (gvns_impl.cuh)
 };
+
+struct GvnsState;
+static void gvns_free(GvnsState *gs);
 
 static int ensure_trace(rl_instance *h, int64_t cap_sweeps, int k_max)
 {
@@ -725,6 +755,7 @@ extern "C" void rl_instance_destroy(rl_instance *h)
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->stream)
         cudaStreamDestroy(h->stream);
+    gvns_free(h->gv);
     delete h;
 }
 
@@ -1245,6 +1276,8 @@ extern "C" int rl_int_peak(double *ops_per_s)
     *ops_per_s = (double)blocks * threads * iters * 4 * 8 * 2 / (best * 1e-3);
     return 0;
 }
+
+#include "gvns_impl.cuh"
 
 extern "C" int64_t rl_launch_count(const rl_instance *h) { return h ? h->launches : 0; }
 

@@ -1,0 +1,126 @@
+"""Device shaking / worker rounds / GVNS vs the live reference's outputs
+(tests/golden/gvns_small.npz, gvns_k1000.json) and the numpy RNG
+restatement (oracle/numpy_rng.py, itself pinned to numpy)."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import numpy_rng
+from conftest import GOLDEN, GoldInstance, golden
+from paper_1704_05132_b200 import (GeneratorConfig, Instance, SetupPlan, SolverConfig,
+                                   generate_instance, gvns, initial_solution, shake, vnd,
+                                   worker_round)
+from paper_1704_05132_b200._native import rng_probe
+from paper_1704_05132_b200.gvns import _worker_rng
+
+pytestmark = pytest.mark.gpu
+
+
+def _inst(data, prefix):
+    g = GoldInstance(data, prefix)
+    return Instance(g.products, g.periods, g.demand, g.returns, g.setup_cost_m,
+                    g.setup_cost_r, g.holding_cost_m, g.holding_cost_r, g.unit_cost_m,
+                    g.unit_cost_r)
+
+
+def _plan_sha(plan):
+    h = hashlib.sha256()
+    h.update(np.packbits(plan.setup_m).tobytes())
+    h.update(np.packbits(plan.setup_r).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("triple", [(0, 0, 0), (7, 5, 0), (2**32 + 5, 1, 1),
+                                    (2**64 - 1, 2**33, 1023), (123456789, 0, 511)])
+@pytest.mark.parametrize("pop,size,shuf", [(104000, 5, 0), (2, 1, 7), (12, 3, 300),
+                                           (20000, 401, 2), (2**33, 3, 1), (10001, 5, 0)])
+def test_device_philox_matches_numpy(triple, pop, size, shuf):
+    raw, pick, sh, tail = rng_probe(*triple, pop, size, shuf)
+    ref = numpy_rng.Philox.from_entropy(triple)
+    assert raw.tolist() == [ref.next64() for _ in range(4)]
+    assert pick.tolist() == ref.choice_noreplace(pop, size)
+    arr = [3 * i + 1 for i in range(shuf)]
+    ref.shuffle(arr)
+    assert sh.tolist() == arr
+    assert tail.tolist() == [ref.next64()]
+
+
+def test_device_philox_matches_live_numpy_choice():
+    for w in range(8):
+        rng = _worker_rng(0, 3, w)
+        rng.bit_generator.random_raw(4)   # the probe draws 4 raw words first
+        want = rng.choice(104000, size=5, replace=False).tolist()
+        assert rng_probe(0, 3, w, 104000, 5, 0)[1].tolist() == want
+
+
+def _small_cases():
+    data = golden("gvns_small.npz")
+    cases = sorted({k.split("_")[0] for k in data.files if k.startswith("s")
+                    and k.split("_")[0][1:].isdigit()})
+    return data, cases
+
+
+def test_public_shake_matches_reference():
+    data, cases = _small_cases()
+    n = 0
+    for key in data["shake_keys"].tolist():
+        ci, pk, kk, s, r, w = key.split("_")
+        inst = _inst(data, ci + "_")
+        inc = initial_solution(inst)
+        plan = inc if pk == "p0" else vnd(inst, inc)[0]
+        got = shake(inst, plan, int(kk[1:]), _worker_rng(int(s), int(r), int(w)))
+        assert np.array_equal(got.setup_m, data[key + "_sm"]), key
+        assert np.array_equal(got.setup_r, data[key + "_sr"]), key
+        n += 1
+    assert n > 100
+
+
+def test_worker_round_matches_reference():
+    data, cases = _small_cases()
+    for ci in cases:
+        inst = _inst(data, ci + "_")
+        inc = initial_solution(inst)
+        plans = (inc, vnd(inst, inc)[0])
+        for W in (1, 2, 3):
+            cfg = SolverConfig(t_max=1e9, k_max=3, workers=W, seed=7, max_rounds=6)
+            for pk, plan in enumerate(plans):
+                for k in (1, 3):
+                    key = f"{ci}_wr_W{W}_p{pk}_k{k}"
+                    got, cost = worker_round(inst, plan, k, cfg, round_index=5)
+                    assert cost == int(data[key + "_cost"]), key
+                    assert np.array_equal(got.setup_m, data[key + "_sm"]), key
+                    assert np.array_equal(got.setup_r, data[key + "_sr"]), key
+
+
+def test_gvns_round_capped_matches_reference():
+    data, cases = _small_cases()
+    for ci in cases:
+        inst = _inst(data, ci + "_")
+        for W in (1, 2, 3):
+            cfg = SolverConfig(t_max=1e9, k_max=3, workers=W, seed=7, max_rounds=6)
+            res = gvns(inst, cfg)
+            key = f"{ci}_gvns_W{W}"
+            assert res.cost == int(data[key + "_cost"]), key
+            assert res.rounds == int(data[key + "_rounds"])
+            assert res.shake_calls == int(data[key + "_shakes"])
+            assert np.array_equal(res.plan.setup_m, data[key + "_sm"]), key
+            assert np.array_equal(res.plan.setup_r, data[key + "_sr"]), key
+
+
+def test_gvns_k1000_matches_reference():
+    """BASELINE config 2 (K=1000, T=52, full GVNS): round-capped runs of the
+    live reference (W=2 x 20 rounds, W=16 x 4 rounds)."""
+    with open(os.path.join(GOLDEN, "gvns_k1000.json")) as f:
+        gold = json.load(f)
+    inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+    for name, (W, R) in (("W2_R20", (2, 20)), ("W16_R4", (16, 4))):
+        cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=W, seed=0, max_rounds=R)
+        res = gvns(inst, cfg)
+        g = gold[name]
+        assert res.cost == g["cost"], name
+        assert res.rounds == g["rounds"] and res.shake_calls == g["shake_calls"]
+        assert _plan_sha(res.plan) == g["plan_sha"], name
