@@ -172,14 +172,15 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1704_05132_b200 import _native
-    from paper_1704_05132_b200 import devbench
+    from paper_1704_05132_b200 import devbench, sharded
 
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     K, T = wl["products"], wl["periods"]
     inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=0))
-    lo, hi = K * rank // world, K * (rank + 1) // world
+    from paper_1704_05132_b200.sharded import shard_bounds
+    lo, hi = shard_bounds(K, rank, world)
     shard = inst.slice(lo, hi)
     dev = _native.DeviceInstance(shard)
     stream = torch.cuda.Stream()   # a real stream: events and kernels share it
@@ -201,11 +202,14 @@ def main():
     def collect():
         tr = np.empty(1 << 16, np.int64)
         nt = np.zeros(1, np.int64)
-        st = np.zeros(8, np.int64)
+        st = np.zeros(9, np.int64)
         _native.check(_native.load().rl_vnd_collect(dev.h, _native.ptr(tr), len(tr),
                                                     _native.ptr(nt), _native.ptr(st)),
                       "rl_vnd_collect")
-        return st
+        trace = tr[:nt[0]].tolist()
+        stats = dict(evals=int(st[3]), evals_reference=int(st[4]), moves=int(st[5]),
+                     ntot_sum=int(st[8]), k_max=4, kernel_ns=int(st[7]))
+        return trace, stats
 
     for _ in range(args.warmup):
         step()
@@ -227,7 +231,7 @@ def main():
         step()
         e1.record(stream)
         torch.cuda.synchronize()
-        kernel_ms.append(collect()[7] / 1e6)
+        kernel_ms.append(collect()[1]["kernel_ns"] / 1e6)
     torch.cuda.synchronize()
     launches = dev.launches - launches0
     if world > 1:
@@ -235,14 +239,19 @@ def main():
     clocks = sampler.stop()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     my_ms = float(np.sum(step_ms))
-    st = collect()
-    # totals across ranks: time = max, work = sum
-    tot = torch.tensor([st[4], st[3], st[0], st[5], st[2]], dtype=torch.int64, device="cuda")
+    trace, stats = collect()
+    # totals across ranks: time = max over ranks, work = the combined lockstep
+    # counts (sharded.combine rebuilds the global trace and evaluation count)
     tmax = torch.tensor([my_ms, float(np.mean(kernel_ms))], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        g_trace, totals = sharded.combine(trace, stats, device="cuda")
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    ref_evals, done_evals, final_cost, moves, _ = [int(x) for x in tot.tolist()]
+    else:
+        g_trace, totals = trace, dict(evals_reference=stats["evals_reference"],
+                                      evals=stats["evals"], cost=trace[-1],
+                                      moves=stats["moves"])
+    ref_evals, done_evals = totals["evals_reference"], totals["evals"]
+    final_cost, moves = totals["cost"], totals["moves"]
     total_ms, vnd_kernel_ms = tmax.tolist()
     ms_per_step = total_ms / args.steps
 

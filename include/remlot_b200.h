@@ -88,7 +88,8 @@ int rl_list_moves(int nbh, int64_t T, const uint8_t *sm_row, const uint8_t *sr_r
  * exceeds trace_cap only trace_cap are written).  stats[0..7] = final cost,
  * start cost, sweeps, candidate evaluations performed, reference-equivalent
  * evaluations (lockstep count), moves applied, products,
- * kernel time in ns. */
+ * kernel time in ns, sum over feasible products of their final move counts
+ * (stats has 9 entries). */
 int rl_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t *sr_in,
            uint8_t *sm_out, uint8_t *sr_out, int64_t *trace, int64_t trace_cap,
            int64_t *n_trace, int64_t *stats);

@@ -176,7 +176,7 @@ class DeviceInstance:
         while True:
             trace = np.empty(cap, np.int64)
             nt = np.zeros(1, np.int64)
-            st = np.zeros(8, np.int64)
+            st = np.zeros(9, np.int64)
             check(load().rl_vnd(self.h, k_max, ptr(sm), ptr(sr), ptr(out_m.view(np.uint8)),
                                 ptr(out_r.view(np.uint8)), ptr(trace), cap, ptr(nt), ptr(st)),
                   "rl_vnd")
@@ -185,7 +185,7 @@ class DeviceInstance:
             cap = int(nt[0])
         stats = dict(cost=int(st[0]), start_cost=int(st[1]), sweeps=int(st[2]),
                      evals=int(st[3]), evals_reference=int(st[4]), moves=int(st[5]),
-                     products=int(st[6]), kernel_ns=int(st[7]))
+                     products=int(st[6]), kernel_ns=int(st[7]), ntot_sum=int(st[8]))
         return out_m, out_r, trace[:nt[0]].copy(), stats
 
     def decode(self, sm, sr):

@@ -421,6 +421,7 @@ __global__ void k_vnd_finalize(int64_t K, VndOut o, int64_t *summary)
         summary[6] = K;
         summary[8] = *o.overflow;
         summary[9] = r[1];
+        summary[10] = r[4];
     }
 }
 
@@ -1055,6 +1056,7 @@ extern "C" int rl_vnd_collect(rl_instance *h, int64_t *trace, int64_t trace_cap,
     stats[5] = sum[5];
     stats[6] = sum[6];
     stats[7] = (int64_t)((double)ms * 1e6);
+    stats[8] = sum[10];
     return 0;
 }
 

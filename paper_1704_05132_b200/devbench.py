@@ -43,7 +43,7 @@ def e2e_steps(torch, _native, dev, shard, steps, world, dist):
     keep += [tm, tr_, to, tq]
     trace = np.empty(1 << 16, np.int64)
     nt = np.zeros(1, np.int64)
-    st = np.zeros(8, np.int64)
+    st = np.zeros(9, np.int64)
     P = _native.ptr
 
     def one():

@@ -1,0 +1,98 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): product sharding and
+the totals/trace combine of paper_1704_05132_b200.sharded, with the CPU
+oracle as each rank's local descent, must equal one unsharded reference
+descent bit for bit (trace, cost, plan, lockstep evaluation count)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from conftest import ROOT
+from paper_1704_05132_b200.model import GeneratorConfig, generate_instance
+from paper_1704_05132_b200.plan import SetupPlan
+from paper_1704_05132_b200.sharded import shard_bounds, sharded_vnd
+
+
+def _oracle_local_vnd(shard, sm, sr, k_max):
+    m, r, cost, trace, st = oracle.vnd(shard, sm, sr, k_max)
+    feas = oracle.product_costs(shard, m, r) != oracle.INFEASIBLE
+    ntot = 0
+    for k in np.flatnonzero(feas):
+        for nbh in range(1, k_max + 1):
+            ntot += len(oracle.list_moves(nbh, m[k], r[k])[0])
+    return m, r, trace.tolist(), dict(evals=st["evals"], moves=st["moves"],
+                                      evals_reference=st["evals"], ntot_sum=ntot)
+
+
+def _worker(rank, world, port, cases, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = []
+        for K, T, seed, plan_kind in cases:
+            inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=seed,
+                                                     demand_max=30 if T < 20 else 100))
+            if plan_kind == "init":
+                sm, sr = oracle.initial_solution(inst)
+            else:
+                rng = np.random.default_rng(seed)
+                sm, sr = rng.random((K, T)) < 0.5, rng.random((K, T)) < 0.5
+            plan, cost, trace, tot = sharded_vnd(inst, SetupPlan(sm, sr), 4,
+                                                 local_vnd=_oracle_local_vnd)
+            res.append((cost, trace, tot["evals_reference"], tot["moves"], tot["sweeps"],
+                        np.packbits(plan.setup_m).tobytes(), np.packbits(plan.setup_r).tobytes()))
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CASES = [(7, 9, 1, "init"), (13, 52, 0, "init"), (5, 6, 3, "random"), (1, 8, 4, "init")]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_vnd_equals_unsharded_reference(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for i, (K, T, seed, kind) in enumerate(CASES):
+        inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=seed,
+                                                 demand_max=30 if T < 20 else 100))
+        if kind == "init":
+            sm, sr = oracle.initial_solution(inst)
+        else:
+            rng = np.random.default_rng(seed)
+            sm, sr = rng.random((K, T)) < 0.5, rng.random((K, T)) < 0.5
+        m, r, cost, trace, st = oracle.vnd(inst, sm, sr)
+        for rank in range(world):
+            gcost, gtrace, gref, gmoves, gsweeps, pm, pr = got[rank][i]
+            assert gcost == cost
+            assert gtrace == trace.tolist()
+            assert gref == st["evals"]
+            assert gmoves == st["moves"] and gsweeps == st["sweeps"]
+            assert pm == np.packbits(m).tobytes() and pr == np.packbits(r).tobytes()
+
+
+def test_shard_bounds_cover_products_in_order():
+    for K in (1, 5, 100000):
+        for world in (1, 2, 3, 8):
+            spans = [shard_bounds(K, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == K
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
