@@ -7,6 +7,8 @@
 //   cd[T+1]     cd[t] = sum_{i<t} D[i]       (V)
 //   cr[T+1]     cr[t] = sum_{i<t} R[i]       (V)
 //   xin[T]      cumulative remanufactured quantity entering setup u (V)
+//   slk[T]      remanufacturing slack CR[u] - xin[u] - seg(u) at sR setups (V)
+//   lm[17]      T <= 64: masks of sR setups with slack < 2^j (j < 16), slack < 0
 //   cpre[T]     sum of segment costs before setup u (C)
 //   bm[NW],br[NW]  setup bit rows (uint32 words; used when T > 64)
 //   mv[2T+2]    compacted move slots of the current neighborhood (uint16)
@@ -32,6 +34,7 @@
 // for the final values), else int64.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 namespace rl {
 
@@ -48,12 +51,15 @@ struct ProductCosts {
 
 template <typename V, typename C>
 struct Slot {
-    V *stage, *cd, *cr, *xin;
+    V *stage, *cd, *cr, *xin, *slk;
     C *cpre;
     uint32_t *bm, *br;
     uint16_t *mv;
+    uint64_t *lm;
     uint64_t *bar;
 };
+
+constexpr int kSlackLevels = 16;   // lm[j] = {sR setups: slack < 2^j}, lm[16] = {slack < 0}
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -66,9 +72,11 @@ __host__ __device__ inline size_t slot_bytes(int T)
     b += align16((size_t)(T + 1) * sizeof(V));   // cd
     b += align16((size_t)(T + 1) * sizeof(V));   // cr
     b += align16((size_t)T * sizeof(V));         // xin
+    b += align16((size_t)T * sizeof(V));         // slk
     b += align16((size_t)T * sizeof(C));         // cpre
     b += align16(2 * (size_t)NW * sizeof(uint32_t));
     b += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
+    b += align16((kSlackLevels + 1) * 8);        // lm
     b += 16;                                     // mbarrier
     return b;
 }
@@ -83,10 +91,12 @@ __device__ inline Slot<V, C> carve(unsigned char *base, int T)
     s.cd = (V *)p;    p += align16((size_t)(T + 1) * sizeof(V));
     s.cr = (V *)p;    p += align16((size_t)(T + 1) * sizeof(V));
     s.xin = (V *)p;   p += align16((size_t)T * sizeof(V));
+    s.slk = (V *)p;   p += align16((size_t)T * sizeof(V));
     s.cpre = (C *)p;  p += align16((size_t)T * sizeof(C));
     s.bm = (uint32_t *)p;
     s.br = s.bm + NW; p += align16(2 * (size_t)NW * sizeof(uint32_t));
     s.mv = (uint16_t *)p; p += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
+    s.lm = (uint64_t *)p; p += align16((kSlackLevels + 1) * 8);
     s.bar = (uint64_t *)p;
     return s;
 }
@@ -190,6 +200,7 @@ struct MaskSmem {
         }
     }
     __device__ void sync() const { __syncwarp(); }
+    __device__ uint64_t R_mask() const { return 0; }   // unused (no skip for T > 64)
 };
 
 // The rows of a candidate move: base rows with periods a <= b rewritten.
@@ -226,6 +237,7 @@ struct MaskReg {
         return w ? x + __ffsll((long long)w) - 1 : T;
     }
     __device__ int next(int x) const { return next_of(M | R, x, T); }
+    __device__ uint64_t R_mask() const { return R; }
     __device__ int prev(int x) const
     {
         if (x <= 0)
@@ -428,15 +440,20 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
     V pa = __shfl_up_sync(FULL, A, 1), pb = __shfl_up_sync(FULL, B, 1);
     V X = lane == 0 ? V(0) : vmin<V>(pa, pb);
 
+    constexpr bool kSkip = std::is_same<Mask, MaskReg>::value;
     C local = 0;
     bool ok = true;
     for (int u = lo; u < hi; ++u) {
         const bool m = mk.m(u), r = mk.r(u);
+        if (kSkip)
+            s.slk[u] = INF;
         if (!(m | r))
             continue;
         const int v = mk.next(u + 1);
         s.xin[u] = X;
         s.cpre[u] = local;
+        if (kSkip && r)
+            s.slk[u] = s.cr[u + 1] - X - (s.cd[v] - s.cd[u]);
         C c;
         V xr;
         ok &= seg_cost<V, C>(s.cd, s.cr, T, u, v, m, r, X, pc, c, xr);
@@ -459,6 +476,24 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
     const int f = mk.next(0);
     ok = ok && s.cd[f] == 0;   // demand before the first setup (_kernels.py:58-60)
     const bool feas = __all_sync(FULL, ok);
+    if (kSkip) {
+        // slack-level masks for the delta-walk skip (scan_pass): lane l owns
+        // periods l and l + 32, so each ballot yields one 32-bit half
+        __syncwarp();
+        const V s0 = lane < T ? s.slk[lane] : INF;
+        const V s1 = lane + 32 < T ? s.slk[lane + 32] : INF;
+        uint64_t mine = 0;
+#pragma unroll
+        for (int j = 0; j <= kSlackLevels; ++j) {
+            const V lim = j < kSlackLevels ? (V(1) << j) : V(0);
+            const uint64_t mk2 = (uint64_t)__ballot_sync(FULL, s0 < lim) |
+                                 ((uint64_t)__ballot_sync(FULL, s1 < lim) << 32);
+            if (lane == j)
+                mine = mk2;
+        }
+        if (lane <= kSlackLevels)
+            s.lm[lane] = mine;
+    }
     __syncwarp();
     return feas;
 }
@@ -670,26 +705,54 @@ __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int 
             }
         }
         if (act) {
-            const int u = w.u, v = w.nw.next(u + 1);
-            C c;
-            V xr;
-            if (!seg_cost<V, C>(s.cd, s.cr, T, u, v, w.nw.m(u), w.nw.r(u), w.X, pc, c, xr)) {
-                act = false;
-            } else {
-                w.acc += c;
-                w.X += xr;
-                w.u = v;
-                bool done = v >= T;
-                if (!done && v > w.b && w.X == s.xin[v]) {
-                    w.acc += S - s.cpre[v];
-                    done = true;
+            int u = w.u;
+            bool done = false;
+            if (std::is_same<Mask, MaskReg>::value) {
+                // Past the move (u > b) the rows equal the base plan's and
+                // only the entering X differs (delta != 0).  A segment then
+                // costs what it costs in the base plan unless it starts at an
+                // sR setup whose slack < max(delta, 0) (its min(seg, avail)
+                // changes).  Jump to the next setup in the slack-level mask
+                // that bounds that set (false positives are merely evaluated
+                // exactly) and add the base cost of the skipped segments.
+                // Written branch-free: lanes still inside the move keep q = u.
+                const bool ph2 = u > w.b;
+                const V delta = w.X - s.xin[u];
+                const int j = delta <= 1 ? 0 : 64 - __clzll((long long)(uint64_t)(delta - 1));
+                const uint64_t cand = delta < 0 ? s.lm[kSlackLevels]
+                                      : j < kSlackLevels ? s.lm[j] : mk.R_mask();
+                const int q = ph2 ? MaskReg::next_of(cand, u, T) : u;
+                const int qq = q < T ? q : u;
+                const C skipped = (q < T ? s.cpre[qq] : S) - s.cpre[u];
+                if (ph2) {
+                    w.acc += skipped;
+                    w.X = s.xin[qq] + delta;
                 }
-                if (done) {
+                done = q >= T;
+                u = qq;
+            }
+            if (!done) {
+                const int v = w.nw.next(u + 1);
+                C c;
+                V xr;
+                if (!seg_cost<V, C>(s.cd, s.cr, T, u, v, w.nw.m(u), w.nw.r(u), w.X, pc, c, xr)) {
                     act = false;
-                    if (w.acc < best) {
-                        best = w.acc;
-                        key = w.slot;
+                } else {
+                    w.acc += c;
+                    w.X += xr;
+                    w.u = v;
+                    done = v >= T;
+                    if (!done && v > w.b && w.X == s.xin[v]) {
+                        w.acc += S - s.cpre[v];
+                        done = true;
                     }
+                }
+            }
+            if (done) {
+                act = false;
+                if (w.acc < best) {
+                    best = w.acc;
+                    key = w.slot;
                 }
             }
         }
