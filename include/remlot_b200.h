@@ -115,10 +115,11 @@ int rl_decode(rl_instance *h, const uint8_t *sm, const uint8_t *sr, int64_t *x_m
 /* ---- device GVNS (reference gvns.py:88-244) ----------------------------
  * rl_gvns_begin uploads an incumbent plan (must be feasible), computes the
  * lot-for-lot start and F = the VND image of the incumbent, sets strength 1.
- * workers = W, k_max = shake strength bound, k_vnd_max in 1..4, seed = the
- * solver seed (used mod 2^64 like gvns.py:89).  *inc_cost = evaluate(inc). */
-int rl_gvns_begin(rl_instance *h, int workers, int k_max, int k_vnd_max, uint64_t seed,
-                  const uint8_t *sm, const uint8_t *sr, int64_t *inc_cost);
+ * workers = W local workers with global indices worker_offset.., k_max =
+ * shake strength bound, k_vnd_max in 1..4, seed = the solver seed (used mod
+ * 2^64 like gvns.py:89).  *inc_cost = evaluate(inc). */
+int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset, int k_max, int k_vnd_max,
+                  uint64_t seed, const uint8_t *sm, const uint8_t *sr, int64_t *inc_cost);
 /* Overwrite the shake strength k (worker_round(..., k, ...)). */
 int rl_gvns_set_strength(rl_instance *h, int64_t strength);
 /* One round (worker_round, gvns.py:147-174) with round index round_index;
@@ -129,6 +130,14 @@ int rl_gvns_round(rl_instance *h, int64_t round_index, int accept);
  * info[0..5] = incumbent cost, strength, last best cost, last best worker,
  * accepted rounds, shake fallbacks in the last round.  sm/sr may be NULL. */
 int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr, int64_t *info);
+/* Sharded rounds (one rank per GPU, workers split in blocks): after
+ * rl_gvns_round(h, r, 0), rl_gvns_candidate copies this rank's winning
+ * candidate plan (2KT bytes: m rows then r rows) to device memory d_plan
+ * (may be NULL) and writes best[0] = its cost, best[1] = its global worker;
+ * rl_gvns_import(h, d_plan, cost) makes the job's winner (a VND fixpoint,
+ * device memory) the incumbent. */
+int rl_gvns_candidate(rl_instance *h, uint8_t *d_plan, int64_t *best);
+int rl_gvns_import(rl_instance *h, const uint8_t *d_plan, int64_t cost);
 /* Test hook: numpy-exact Philox stream of SeedSequence((seed, round,
  * worker)) on the device: out = 4 raw next64, choice(pop, size,
  * replace=False), shuffle of [1, 4, 7, ...] (shuffle_n), one more next64. */

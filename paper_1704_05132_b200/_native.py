@@ -23,7 +23,8 @@ EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_instance_info", "rl_product_costs", "rl_scan_products", "rl_apply_scan",
            "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect",
            "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
-           "rl_gvns_round", "rl_gvns_state", "rl_rng_probe", "rl_launch_count",
+           "rl_gvns_round", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
+           "rl_rng_probe", "rl_launch_count",
            "rl_last_error")
 
 _lib = None
@@ -62,7 +63,9 @@ def load():
         "rl_initial_solution_device": (I, [P, P, P, P]),
         "rl_decode": (I, [P] + [P] * 7),
         "rl_int_peak": (I, [P]),
-        "rl_gvns_begin": (I, [P, I, I, I, ctypes.c_uint64, P, P, P]),
+        "rl_gvns_begin": (I, [P, I, I64, I, I, ctypes.c_uint64, P, P, P]),
+        "rl_gvns_candidate": (I, [P, P, P]),
+        "rl_gvns_import": (I, [P, P, I64]),
         "rl_gvns_set_strength": (I, [P, I64]),
         "rl_gvns_round": (I, [P, I64, I]),
         "rl_gvns_state": (I, [P, I, P, P, P]),
@@ -197,12 +200,24 @@ class DeviceInstance:
         return outs[0], outs[1], outs[2], outs[3], cost
 
     # ---- device GVNS (gvns_impl.cuh)
-    def gvns_begin(self, workers, k_max, k_vnd_max, seed, sm, sr):
+    def gvns_begin(self, workers, k_max, k_vnd_max, seed, sm, sr, worker_offset=0):
         sm, sr = u8(sm), u8(sr)
         cost = np.zeros(1, np.int64)
-        check(load().rl_gvns_begin(self.h, workers, k_max, k_vnd_max, seed & ((1 << 64) - 1),
-                                   ptr(sm), ptr(sr), ptr(cost)), "rl_gvns_begin")
+        check(load().rl_gvns_begin(self.h, workers, worker_offset, k_max, k_vnd_max,
+                                   seed & ((1 << 64) - 1), ptr(sm), ptr(sr), ptr(cost)),
+              "rl_gvns_begin")
         return int(cost[0])
+
+    def gvns_candidate(self, d_plan_ptr):
+        """(cost, global worker) of this rank's best candidate; copies the plan
+        to device memory at d_plan_ptr (int address, 2KT bytes) if given."""
+        best = np.zeros(2, np.int64)
+        check(load().rl_gvns_candidate(self.h, ctypes.c_void_p(d_plan_ptr) if d_plan_ptr else None,
+                                       ptr(best)), "rl_gvns_candidate")
+        return int(best[0]), int(best[1])
+
+    def gvns_import(self, d_plan_ptr, cost):
+        check(load().rl_gvns_import(self.h, ctypes.c_void_p(d_plan_ptr), cost), "rl_gvns_import")
 
     def gvns_set_strength(self, k):
         check(load().rl_gvns_set_strength(self.h, k), "rl_gvns_set_strength")

@@ -16,6 +16,7 @@
 
 struct GvnsArgs {
     int64_t K, KT, pop;
+    int64_t w0;                       // global index of local worker 0 (sharded rounds)
     int T, NW, W, k_max, kcap, tcap, tsize, fb_slots;
     uint64_t seed;
     uint8_t *inc, *F, *init, *cand;   // 2KT bytes each: m rows then r rows
@@ -87,7 +88,7 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
     if (w >= g.W)
         return;
     Philox rng;
-    rng.seed(g.seed, (uint64_t)round, (uint64_t)w);
+    rng.seed(g.seed, (uint64_t)round, (uint64_t)(g.w0 + w));
     const int64_t strength = g.scal[GV_STRENGTH];
     const int64_t k_eff = strength < g.pop ? strength : g.pop;   // gvns.py:113
     int64_t *P = g.pos + (int64_t)w * g.kcap;
@@ -333,7 +334,7 @@ __global__ void k_gvns_join(GvnsArgs g, int mode)
                 s_w[0] = s_w[i];
             }
         g.scal[GV_BEST_COST] = s_cost[0];
-        g.scal[GV_BEST_W] = s_w[0];
+        g.scal[GV_BEST_W] = g.w0 + s_w[0];
         int acc = 0;
         if (mode == 1) {
             acc = s_cost[0] < g.scal[GV_INC_COST];
@@ -452,12 +453,13 @@ static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round)
     return 0;
 }
 
-extern "C" int rl_gvns_begin(rl_instance *h, int workers, int k_max, int k_vnd_max,
-                             uint64_t seed, const uint8_t *sm, const uint8_t *sr,
+extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset, int k_max,
+                             int k_vnd_max, uint64_t seed, const uint8_t *sm, const uint8_t *sr,
                              int64_t *inc_cost)
 {
     (void)cudaGetLastError();
-    if (!h || !sm || !sr || workers < 1 || k_max < 1 || k_vnd_max < 1 || k_vnd_max > 4)
+    if (!h || !sm || !sr || workers < 1 || worker_offset < 0 || k_max < 1 || k_vnd_max < 1 ||
+        k_vnd_max > 4)
         return fail(RL_EINVAL, "rl_gvns_begin: bad arguments (workers=%d k_max=%d k_vnd_max=%d)",
                     workers, k_max, k_vnd_max);
     CK(cudaSetDevice(h->device));
@@ -518,6 +520,7 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int k_max, int k_vnd_m
     }
     GvnsArgs &a = gs->a;
     a.seed = seed;
+    a.w0 = worker_offset;
     gs->k_vnd_max = k_vnd_max;
     // incumbent, lot-for-lot start, and F = per-product VND image of the incumbent
     CK(cudaMemcpyAsync(a.inc, sm, KT, cudaMemcpyHostToDevice, h->stream));
@@ -599,6 +602,53 @@ extern "C" int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr
     info[3] = scal[GV_BEST_W];
     info[4] = scal[GV_ACCEPTED];
     info[5] = scal[GV_FB_COUNT];
+    return 0;
+}
+
+// Sharded rounds (BASELINE config 5): each rank runs a
+// contiguous block of workers; the job joins the per-rank bests and every rank
+// adopts the global winner.  rl_gvns_candidate copies this rank's best
+// candidate (after rl_gvns_round(accept = 0)) to a device buffer (2KT bytes,
+// m rows then r rows) and returns (cost, global worker) on the host;
+// rl_gvns_import makes a plan (a VND fixpoint) the incumbent and its own F.
+extern "C" int rl_gvns_candidate(rl_instance *h, uint8_t *d_plan, int64_t *best)
+{
+    (void)cudaGetLastError();
+    if (!h || !h->gv || !best)
+        return fail(RL_EINVAL, "rl_gvns_candidate: bad arguments");
+    CK(cudaSetDevice(h->device));
+    GvnsArgs &a = h->gv->a;
+    int64_t scal[GV_FBCOST0];
+    if (d_plan)
+        CK(cudaMemcpyAsync(d_plan, a.cand, 2 * a.KT, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(scal, a.scal, sizeof scal, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (scal[GV_ERROR])
+        return fail(RL_ECUDA, "gvns: more shake fallbacks in one round than slots (%d)",
+                    a.fb_slots);
+    best[0] = scal[GV_BEST_COST];
+    best[1] = scal[GV_BEST_W];
+    return 0;
+}
+
+extern "C" int rl_gvns_import(rl_instance *h, const uint8_t *d_plan, int64_t cost)
+{
+    (void)cudaGetLastError();
+    if (!h || !h->gv || !d_plan)
+        return fail(RL_EINVAL, "rl_gvns_import: bad arguments");
+    CK(cudaSetDevice(h->device));
+    GvnsArgs &a = h->gv->a;
+    CK(cudaMemcpyAsync(a.inc, d_plan, 2 * a.KT, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(a.F, d_plan, 2 * a.KT, cudaMemcpyDeviceToDevice, h->stream));
+    const size_t kt = (size_t)a.KT;
+    CK(cudaMemcpyAsync(h->plan, d_plan, 2 * kt, cudaMemcpyDeviceToDevice, h->stream));
+    int rc = RL_DISPATCH_M(h, do_costs, h, (int64_t)0, h->K, a.Fcost);
+    if (rc)
+        return rc;
+    int64_t scal[4] = {cost, cost, 0, 1};   // inc cost, Ftot, (strength kept), inc_is_F
+    CK(cudaMemcpyAsync(&a.scal[GV_INC_COST], &scal[0], 16, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(&a.scal[GV_INC_IS_F], &scal[3], 8, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     return 0;
 }
 

@@ -102,3 +102,101 @@ def sharded_vnd(inst, plan, k_max=4, group=None, local_vnd=None, device="cpu",
         from .plan import SetupPlan
         full = SetupPlan(m, r)
     return full, totals["cost"], g_trace, totals
+
+
+# ---------------------------------------------------------------- replicas
+
+class DeviceRounds:
+    """Round backend of ``sharded_gvns`` on this rank's GPU (gvns_impl.cuh)."""
+
+    def __init__(self, inst):
+        import torch
+        from . import _native
+        self.torch = torch
+        self.dev = _native.DeviceInstance(inst)
+        self.KT = inst.products * inst.periods
+        self.buf = torch.empty(2 * self.KT, dtype=torch.uint8, device="cuda")
+        self.device = "cuda"
+
+    def begin(self, workers, worker_offset, config, sm, sr):
+        return self.dev.gvns_begin(workers, config.k_max, config.k_vnd_max, config.seed, sm, sr,
+                                   worker_offset=worker_offset)
+
+    def round(self, round_index, strength):
+        self.dev.gvns_set_strength(strength)
+        self.dev.gvns_round(round_index, accept=False)
+        cost, w = self.dev.gvns_candidate(self.buf.data_ptr())
+        return cost, w, self.buf
+
+    def adopt(self, plan_tensor, cost):
+        self.dev.gvns_import(plan_tensor.data_ptr(), cost)
+
+    def incumbent(self):
+        sm, sr, info = self.dev.gvns_state(0)
+        return sm, sr
+
+
+def sharded_gvns(inst, config, group=None, backend=None, start_plan=None):
+    """GVNS whose W workers are split in contiguous blocks over the ranks
+    (BASELINE config 5: 1,024 replicas over 8 GPUs).  Every round each rank
+    runs its block, the job all-gathers the per-rank bests (cost, global
+    worker) and takes the minimum (lowest worker on ties, gvns.py:170-174),
+    the winning rank broadcasts its candidate plan, and every rank applies
+    the acceptance and strength step (gvns.py:207-215) identically.  The
+    wall-clock budget is decided on rank 0 and broadcast each round.
+    Returns the reference's GvnsResult on every rank."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from .gvns import GvnsResult, next_strength
+    from .plan import SetupPlan
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    be = backend if backend is not None else DeviceRounds(inst)
+    dev = getattr(be, "device", "cpu")
+    W = config.workers
+    w_lo, w_hi = shard_bounds(W, rank, world)
+    start = time.monotonic()
+    if start_plan is None:
+        if hasattr(be, "initial_solution"):
+            sm0, sr0 = be.initial_solution()
+        else:
+            from .plan import initial_solution
+            p = initial_solution(inst)
+            sm0, sr0 = p.setup_m, p.setup_r
+    else:
+        sm0, sr0 = start_plan.setup_m, start_plan.setup_r
+    local = w_hi - w_lo
+    inc_cost = be.begin(max(local, 1), w_lo, config, sm0, sr0)
+    strength, rounds = 1, 0
+    BIG = (1 << 63) - 1
+    while True:
+        go = torch.tensor([1], dtype=torch.int64, device=dev)
+        if rank == 0:
+            if time.monotonic() - start > config.t_max or (
+                    config.max_rounds is not None and rounds >= config.max_rounds):
+                go[0] = 0
+        dist.broadcast(go, src=0, group=group)
+        if int(go[0]) == 0:
+            break
+        cost, w, plan = be.round(rounds, strength)
+        if local == 0:
+            cost, w = BIG, BIG
+        mine = torch.tensor([cost, w], dtype=torch.int64, device=dev)
+        allb = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(allb, mine, group=group)
+        pairs = [tuple(int(x) for x in t.tolist()) for t in allb]
+        best_cost, best_w = min(pairs)
+        src = min(r for r in range(world) if pairs[r] == (best_cost, best_w))
+        improved = best_cost < inc_cost
+        if improved:
+            dist.broadcast(plan, src=src, group=group)
+            be.adopt(plan, best_cost)
+            inc_cost = best_cost
+        strength = next_strength(strength, improved, config.k_max)
+        rounds += 1
+    sm, sr = be.incumbent()
+    return GvnsResult(SetupPlan(sm, sr), inc_cost, rounds, time.monotonic() - start,
+                      rounds * W)

@@ -96,3 +96,52 @@ def test_shard_bounds_cover_products_in_order():
             spans = [shard_bounds(K, r, world) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == K
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def _gvns_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from gvns_oracle import OracleRounds
+        from paper_1704_05132_b200.gvns import SolverConfig
+        from paper_1704_05132_b200.model import Instance
+        from paper_1704_05132_b200.sharded import sharded_gvns
+        from conftest import GoldInstance, golden
+        data = golden("gvns_small.npz")
+        res = []
+        for ci in ("s0", "s3", "s5", "s7"):
+            g = GoldInstance(data, ci + "_")
+            inst = Instance(g.products, g.periods, g.demand, g.returns, g.setup_cost_m,
+                            g.setup_cost_r, g.holding_cost_m, g.holding_cost_r,
+                            g.unit_cost_m, g.unit_cost_r)
+            cfg = SolverConfig(t_max=1e9, k_max=3, workers=3, seed=7, max_rounds=6)
+            r = sharded_gvns(inst, cfg, backend=OracleRounds(inst))
+            res.append((ci, r.cost, r.rounds, r.shake_calls, r.plan.setup_m.tobytes(),
+                        r.plan.setup_r.tobytes()))
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_replicas_equal_reference_gvns(world):
+    """Workers split over ranks (BASELINE config 5 shape): the cross-rank
+    best-of join reproduces the reference gvns() (W=3, 6 rounds) exactly."""
+    from conftest import golden
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gvns_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    data = golden("gvns_small.npz")
+    for rank in range(world):
+        for ci, cost, rounds, shakes, pm, pr in got[rank]:
+            key = f"{ci}_gvns_W3"
+            assert cost == int(data[key + "_cost"]), key
+            assert rounds == 6 and shakes == 18
+            assert pm == data[key + "_sm"].tobytes() and pr == data[key + "_sr"].tobytes(), key

@@ -124,3 +124,30 @@ def test_gvns_k1000_matches_reference():
         assert res.cost == g["cost"], name
         assert res.rounds == g["rounds"] and res.shake_calls == g["shake_calls"]
         assert _plan_sha(res.plan) == g["plan_sha"], name
+
+
+def test_sharded_replicas_device_backend_single_rank():
+    """The replica-sharded driver on the device backend (candidate export,
+    NCCL all-gather/broadcast, import) reproduces the reference's K=1000
+    W=16 GVNS with one rank; multi-rank splits are covered on gloo."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_1704_05132_b200.sharded import sharded_gvns
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        with open(os.path.join(GOLDEN, "gvns_k1000.json")) as f:
+            g = json.load(f)["W16_R4"]
+        inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+        cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=16, seed=0, max_rounds=4)
+        res = sharded_gvns(inst, cfg)
+        assert res.cost == g["cost"] and res.rounds == 4 and res.shake_calls == 64
+        assert _plan_sha(res.plan) == g["plan_sha"]
+    finally:
+        dist.destroy_process_group()
