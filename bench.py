@@ -131,6 +131,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=20000,
                     help="products of the instance timed on the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the secondary configs (C2 GVNS, C4, C5 share)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -303,6 +305,11 @@ def main():
                 "value": r["value"], "unit": "evals/s", "cores": threads, "kind": "port",
                 "sample": f"first {sample} products, lockstep VND to local optimum "
                           f"({r['seconds_per_step']:.2f} s)"}
+        if world == 1 and not args.no_extra:
+            line["other_configs"] = devbench.other_configs(torch)
+        if args.workload == "c3" and world == 1:
+            line["parity"] = {"final_cost": final_cost, "reference_final_cost": 449100704810,
+                              "bit_exact": final_cost == 449100704810}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

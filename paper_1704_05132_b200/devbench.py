@@ -69,3 +69,50 @@ def e2e_steps(torch, _native, dev, shard, steps, world, dist):
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         dist.all_reduce(byt, op=dist.ReduceOp.SUM)
     return float(tot[0]), int(byt[0]), int(byt[1])
+
+
+def other_configs(torch):
+    """Secondary BASELINE configs measured on this GPU (reported beside the
+    headline; each parity-checked where a reference golden exists):
+      c2_vnd  K=1000 T=52 VND to local optimum (ms; golden cost 4,484,593,955)
+      c2_gvns K=1000 T=52 full GVNS, W=2, k_max=5: rounds/s over 400 rounds
+      c4_vnd  K=10000 T=520 VND to local optimum (ms)
+      c5_gvns K=1000 T=52, W=128 workers (one GPU's share of 1,024): rounds/s
+    Times are device-synchronised wall clock around the C ABI calls."""
+    from . import _native
+    from .gvns import SolverConfig, gvns
+    from .model import GeneratorConfig, generate_instance
+
+    out = {}
+
+    def vnd_ms(K, T, reps=3):
+        inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=0))
+        dev = _native.device_instance(inst)
+        sm, sr = dev.initial_solution()
+        dev.vnd(sm, sr)
+        best, st = None, None
+        for _ in range(reps):
+            _, _, _, st = dev.vnd(sm, sr)
+            ms = st["kernel_ns"] / 1e6
+            best = ms if best is None else min(best, ms)
+        return inst, best, st
+
+    inst2, ms, st = vnd_ms(1000, 52)
+    out["c2_vnd"] = {"kernel_ms": ms, "cost": st["cost"], "bit_exact": st["cost"] == 4484593955,
+                     "evals_reference": st["evals_reference"]}
+    for name, W, R in (("c2_gvns", 2, 400), ("c5_gvns_1gpu_share", 128, 40)):
+        cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=W, seed=0, max_rounds=R)
+        gvns(inst2, SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=W, seed=0,
+                                 max_rounds=2))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = gvns(inst2, cfg)
+        dt = time.perf_counter() - t0
+        out[name] = {"workers": W, "rounds": res.rounds, "seconds": dt,
+                     "rounds_per_s": res.rounds / dt, "shakes_per_s": res.shake_calls / dt,
+                     "best_cost": res.cost}
+    _, ms, st = vnd_ms(10000, 520, reps=2)
+    out["c4_vnd"] = {"kernel_ms": ms, "cost": st["cost"], "sweeps": st["sweeps"],
+                     "evals_reference": st["evals_reference"],
+                     "reference_equiv_evals_per_s": st["evals_reference"] / (ms / 1e3)}
+    return out
