@@ -49,6 +49,10 @@ int rl_instance_update(rl_instance *h, const int64_t *demand, const int64_t *ret
                        const int64_t *hold_m, const int64_t *hold_r,
                        const int64_t *unit_m, const int64_t *unit_r);
 void rl_instance_destroy(rl_instance *h);
+/* Kernel variant of rl_vnd for T <= 64: packed = 1 runs two products per
+ * warp in lockstep sweeps, 0 (default) one product per warp.  Results are
+ * identical; the switch exists for A/B measurement and tests. */
+int rl_instance_set_variant(rl_instance *h, int packed);
 /* info[0..5] = K, T, bytes per period value (4|8), bytes per cost (4|8),
  * SM count, warps per CTA of the resident VND kernel. */
 int rl_instance_info(const rl_instance *h, int64_t *info);

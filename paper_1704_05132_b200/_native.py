@@ -20,6 +20,7 @@ RL_ERANGE = -4
 
 # every symbol include/remlot_b200.h declares (checked by tests/test_native_lib.py)
 EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
+           "rl_instance_set_variant",
            "rl_instance_info", "rl_product_costs", "rl_scan_products", "rl_apply_scan",
            "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect",
            "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
@@ -52,6 +53,7 @@ def load():
         "rl_instance_update": (I, [P] + [P] * 8),
         "rl_instance_destroy": (None, [P]),
         "rl_instance_info": (I, [P, P]),
+        "rl_instance_set_variant": (I, [P, I]),
         "rl_product_costs": (I, [P, I64, I64, P, P, P]),
         "rl_scan_products": (I, [P, I64, I64, P, P, I] + [P] * 8),
         "rl_apply_scan": (I, [P, I64, I64] + [P] * 10),
@@ -124,6 +126,10 @@ class DeviceInstance:
         if h is not None and _lib is not None:
             _lib.rl_instance_destroy(h)
             self.h = None
+
+    def set_variant(self, packed):
+        """T <= 64: 1 = two products per warp, 0 = one per warp (default)."""
+        check(load().rl_instance_set_variant(self.h, int(packed)), "rl_instance_set_variant")
 
     @property
     def launches(self):

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "../../include/remlot_b200.h"
 #include "rng_device.cuh"
@@ -373,6 +374,8 @@ __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstVie
     }
 }
 
+#include "vnd_packed.cuh"
+
 // Totals (one block).  summary: 0 final, 1 start, 2 sweeps, 3 evals done,
 // 4 reference-equivalent evals, 5 moves, 6 K, 8 overflow, 9 sum of decreases.
 __global__ void k_vnd_finalize(int64_t K, VndOut o, int64_t *summary)
@@ -592,6 +595,8 @@ struct rl_instance {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timing = false;
     struct GvnsState *gv = nullptr;        // device GVNS state (gvns_impl.cuh)
+    bool pack2 = false;                    // T <= 63: two products per warp (vnd_packed.cuh;
+                                           // measured slower, kept for A/B)
 };
 
 struct GvnsState;
@@ -778,6 +783,30 @@ static int launch_cfg(rl_instance *h, const void *fn, int64_t nprod, int &grid, 
     return 0;
 }
 
+template <typename V, typename C>
+static int launch_cfg_pack2(rl_instance *h, const void *fn, int64_t nprod, int &grid, size_t &smem)
+{
+    smem = kWarpsPerCta * 2 * slot_bytes<V, C>(h->T);
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem));
+    if (occ < 1)
+        return fail(RL_EINVAL, "T=%d needs %zu B shared memory per CTA", h->T, smem);
+    const int64_t want = (nprod + 2 * kWarpsPerCta - 1) / (2 * kWarpsPerCta);
+    const int64_t cap = (int64_t)h->sms * occ;
+    grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+    return 0;
+}
+
+extern "C" int rl_instance_set_variant(rl_instance *h, int packed)
+{
+    if (!h || packed < 0 || packed > 1)
+        return fail(RL_EINVAL, "rl_instance_set_variant: bad arguments");
+    h->pack2 = packed != 0;
+    return 0;
+}
+
 extern "C" int rl_instance_info(const rl_instance *h, int64_t *info)
 {
     if (!h || !info)
@@ -809,9 +838,9 @@ static InstView<V> view(rl_instance *h)
      : (h)->vbytes == 4                   ? FN<int32_t, int64_t>(__VA_ARGS__) \
                                           : FN<int64_t, int64_t>(__VA_ARGS__))
 
-// ... and on where the setup rows live (registers for T <= 64)
+// ... and on where the setup rows live (registers for T <= 63)
 #define RL_DISPATCH_M(h, FN, ...)                                                        \
-    ((h)->T <= 64                                                                        \
+    ((h)->T <= 63                                                                        \
          ? ((h)->vbytes == 4 && (h)->cbytes == 4 ? FN<int32_t, int32_t, MaskReg>(__VA_ARGS__)  \
             : (h)->vbytes == 4                   ? FN<int32_t, int64_t, MaskReg>(__VA_ARGS__)  \
                                                  : FN<int64_t, int64_t, MaskReg>(__VA_ARGS__)) \
@@ -975,7 +1004,9 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
 {
     int grid;
     size_t smem;
-    int rc = launch_cfg<V, C>(h, (const void *)k_vnd<V, C, Mask>, h->K, grid, smem);
+    const bool pack = std::is_same<Mask, MaskReg>::value && h->pack2;
+    int rc = pack ? launch_cfg_pack2<V, C>(h, (const void *)k_vnd_pack2<V, C>, h->K, grid, smem)
+                  : launch_cfg<V, C>(h, (const void *)k_vnd<V, C, Mask>, h->K, grid, smem);
     if (rc)
         return rc;
     const int64_t K = h->K;
@@ -993,8 +1024,12 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     CK(cudaMemsetAsync(h->ints, 0, 2 * sizeof(int), st));
     CK(cudaMemsetAsync(h->trace_dec, 0, (size_t)h->cap_sweeps * k_max * 8, st));
     CK(cudaEventRecord(h->ev0, st));
-    k_vnd<V, C, Mask><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out, sr_out,
-                                                        k_max, o);
+    if (pack)
+        k_vnd_pack2<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
+                                                                  sr_out, k_max, o);
+    else
+        k_vnd<V, C, Mask><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
+                                                                  sr_out, k_max, o);
     CKL();
     CK(cudaEventRecord(h->ev1, st));
     k_vnd_finalize<<<1, 1024, 0, st>>>(K, o, h->summary);

@@ -8,12 +8,12 @@
 //   cr[T+1]     cr[t] = sum_{i<t} R[i]       (V)
 //   xin[T]      cumulative remanufactured quantity entering setup u (V)
 //   slk[T]      remanufacturing slack CR[u] - xin[u] - seg(u) at sR setups (V)
-//   lm[17]      T <= 64: masks of sR setups with slack < 2^j (j < 16), slack < 0
+//   lm[17]      T <= 63: masks of sR setups with slack < 2^j (j < 16), slack < 0
 //   cpre[T]     sum of segment costs before setup u (C)
 //   bm[NW],br[NW]  setup bit rows (uint32 words; used when T > 64)
 //   mv[2T+2]    compacted move slots of the current neighborhood (uint16)
 //
-// For T <= 64 the setup rows live in registers instead (two warp-uniform
+// For T <= 63 the setup rows live in registers instead (two warp-uniform
 // uint64 masks, class MaskReg): "next/previous setup" are single bit scans
 // and a candidate move's rows are built with two masked ORs.  For longer
 // horizons MaskSmem scans the shared-memory words.
@@ -223,26 +223,24 @@ struct PatchedSmem {
     }
 };
 
-// Setup rows in two warp-uniform registers (T <= 64).
+// Setup rows in two warp-uniform registers (T <= 63: bit T is a sentinel
+// "setup" so a next-setup query is one bit scan with no empty case).
 struct MaskReg {
     uint64_t M, R;
     int T;
     __device__ bool m(int t) const { return (M >> t) & 1; }
     __device__ bool r(int t) const { return (R >> t) & 1; }
-    __device__ static int next_of(uint64_t S, int x, int T)
+    // smallest set bit >= x of S (which carries the sentinel bit T), x <= T
+    __device__ static int next_of(uint64_t S, int x, int)
     {
-        if (x >= T)
-            return T;
-        const uint64_t w = S >> x;
-        return w ? x + __ffsll((long long)w) - 1 : T;
+        return x + __ffsll((long long)(S >> x)) - 1;
     }
-    __device__ int next(int x) const { return next_of(M | R, x, T); }
+    __device__ uint64_t sentinel() const { return 1ull << T; }
+    __device__ int next(int x) const { return next_of(M | R | sentinel(), x, T); }
     __device__ uint64_t R_mask() const { return R; }
     __device__ int prev(int x) const
     {
-        if (x <= 0)
-            return -1;
-        const uint64_t w = (M | R) & (x >= 64 ? ~0ull : ((1ull << x) - 1));
+        const uint64_t w = (M | R) & ((1ull << x) - 1);   // x <= T <= 63
         return w ? 63 - __clzll((long long)w) : -1;
     }
     __device__ void set(int t, bool mv, bool rv, int)
@@ -255,19 +253,18 @@ struct MaskReg {
 };
 
 struct PatchedReg {
-    uint64_t M, R;
-    int T;
+    uint64_t M, R, S;   // S = M | R | sentinel
     PatchedReg() = default;
     __device__ PatchedReg(const MaskReg &base, int a, int b, bool ma, bool ra, bool mb, bool rb)
     {
         const uint64_t ba = 1ull << a, bb = 1ull << b, clr = ~(ba | bb);
         M = (base.M & clr) | (ma ? ba : 0) | (mb ? bb : 0);
         R = (base.R & clr) | (ra ? ba : 0) | (rb ? bb : 0);
-        T = base.T;
+        S = M | R | base.sentinel();
     }
     __device__ bool m(int t) const { return (M >> t) & 1; }
     __device__ bool r(int t) const { return (R >> t) & 1; }
-    __device__ int next(int x) const { return MaskReg::next_of(M | R, x, T); }
+    __device__ int next(int x) const { return MaskReg::next_of(S, x, 0); }
 };
 
 template <typename Mask> struct PatchOf;
@@ -559,7 +556,7 @@ __device__ inline bool slot_valid(const Mask &mk, int nbh, int slot, int T)
     if (slot >= 4 * T)
         return false;
     const bool rrow = slot >= 2 * T;
-    const int t = (slot % (2 * T)) >> 1;
+    const int t = (slot - (rrow ? 2 * T : 0)) >> 1;
     auto row = [&](int q) { return rrow ? mk.r(q) : mk.m(q); };
     if (!row(t))
         return false;
@@ -581,7 +578,7 @@ __device__ inline MoveDesc slot_move(const Mask &mk, int nbh, int slot, int T)
         return d;
     }
     const bool rrow = slot >= 2 * T;
-    const int t = (slot % (2 * T)) >> 1;
+    const int t = (slot - (rrow ? 2 * T : 0)) >> 1;
     const int t1 = (slot & 1) ? t + 1 : t - 1;
     d.p0 = t;
     d.p1 = t1;
@@ -719,8 +716,8 @@ __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int 
                 const bool ph2 = u > w.b;
                 const V delta = w.X - s.xin[u];
                 const int j = delta <= 1 ? 0 : 64 - __clzll((long long)(uint64_t)(delta - 1));
-                const uint64_t cand = delta < 0 ? s.lm[kSlackLevels]
-                                      : j < kSlackLevels ? s.lm[j] : mk.R_mask();
+                const uint64_t cand = (delta < 0 ? s.lm[kSlackLevels]
+                                       : j < kSlackLevels ? s.lm[j] : mk.R_mask()) | (1ull << T);
                 const int q = ph2 ? MaskReg::next_of(cand, u, T) : u;
                 const int qq = q < T ? q : u;
                 const C skipped = (q < T ? s.cpre[qq] : S) - s.cpre[u];
