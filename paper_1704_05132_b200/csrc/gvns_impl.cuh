@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, in
         const C K0 = build_prefix(s, T, pc, lane);
         C S0, S;
         VndStats st;
-        vnd_product(s, mk, T, pc, k_vnd_max, lane, S0, S, st, nullptr, 0, nullptr);
+        vnd_product<V, C, Mask, true>(s, mk, T, pc, k_vnd_max, lane, S0, S, st, nullptr, 0,
+                                      nullptr);
         const int64_t cost = (int64_t)(K0 + S);
         if (row) {
             __syncwarp();

@@ -248,7 +248,7 @@ struct VndStats {
 // decreases go to trace_dec[sweep*k_max + nbh-1] when trace_dec != nullptr.
 // Returns the base plan's feasibility (an infeasible product is skipped,
 // _kernels.py:289-290, and counts one sweep).
-template <typename V, typename C, typename Mask>
+template <typename V, typename C, typename Mask, bool Skip>
 __device__ inline bool vnd_product(const Slot<V, C> &s, Mask &mk, int T, const ProductCosts<C> &pc,
                                    int k_max, int lane, C &S0, C &S, VndStats &st,
                                    unsigned long long *trace_dec, int64_t cap_sweeps,
@@ -258,7 +258,7 @@ __device__ inline bool vnd_product(const Slot<V, C> &s, Mask &mk, int T, const P
     st.sweeps = 0;
     st.moves = 0;
     st.ntot = 0;
-    const bool feas = base_pass(s, mk, T, pc, lane, S);
+    const bool feas = base_pass<V, C, Mask, Skip>(s, mk, T, pc, lane, S);
     S0 = S;
     if (!feas) {
         st.sweeps = 1;
@@ -269,11 +269,11 @@ __device__ inline bool vnd_product(const Slot<V, C> &s, Mask &mk, int T, const P
         bool improved = false;
         for (int nbh = 1; nbh <= k_max; ++nbh) {
             if (dirty) {
-                base_pass(s, mk, T, pc, lane, S);
+                base_pass<V, C, Mask, Skip>(s, mk, T, pc, lane, S);
                 dirty = false;
             }
             C best;
-            const PassResult r = scan_pass(s, mk, T, pc, S, nbh, lane, best);
+            const PassResult r = scan_pass<V, C, Mask, Skip>(s, mk, T, pc, S, nbh, lane, best);
             st.evals += r.n_moves;
             if (r.improved) {
                 apply_slot(mk, nbh, r.slot, T, lane);
@@ -317,13 +317,13 @@ struct VndOut {
 // CTAs per SM the register allocation must allow (register-light int32 /
 // register-mask variant runs 6 x 4 warps per SM; measured).
 template <typename V, typename C, typename Mask> struct VndMinBlocks { static constexpr int value = 1; };
-template <> struct VndMinBlocks<int32_t, int32_t, MaskReg> { static constexpr int value = 6; };
+template <> struct VndMinBlocks<int32_t, int32_t, MaskReg> { static constexpr int value = 7; };
 #ifdef RL_VND_MINB
 #define RL_VND_MINB_OF(V, C, M) RL_VND_MINB
 #else
 #define RL_VND_MINB_OF(V, C, M) VndMinBlocks<V, C, M>::value
 #endif
-template <typename V, typename C, typename Mask>
+template <typename V, typename C, typename Mask, bool Skip>
 __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstView<V> in, const uint8_t *sm_in,
                                              const uint8_t *sr_in, uint8_t *sm_out,
                                              uint8_t *sr_out, int k_max, VndOut o)
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstVie
 
         C S, S0;
         VndStats st;
-        const bool feas = vnd_product(s, mk, T, pc, k_max, lane, S0, S, st, o.trace_dec,
+        const bool feas = vnd_product<V, C, Mask, Skip>(s, mk, T, pc, k_max, lane, S0, S, st, o.trace_dec,
                                       o.cap_sweeps, o.overflow);
         store_rows(mk, sm_out, sr_out, k, T, lane);
         if (lane == 0) {
@@ -1005,8 +1005,14 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     int grid;
     size_t smem;
     const bool pack = std::is_same<Mask, MaskReg>::value && h->pack2;
-    int rc = pack ? launch_cfg_pack2<V, C>(h, (const void *)k_vnd_pack2<V, C>, h->K, grid, smem)
-                  : launch_cfg<V, C>(h, (const void *)k_vnd<V, C, Mask>, h->K, grid, smem);
+    // skip pays when the launch is latency-bound: fewer products than ~2
+    // waves of resident warps (C2, GVNS) -- measured, DESIGN.md section 5
+    const bool skip = std::is_same<Mask, MaskReg>::value && h->K < (int64_t)h->sms * 64;
+    const void *fn = pack ? (const void *)k_vnd_pack2<V, C>
+                     : skip ? (const void *)k_vnd<V, C, Mask, true>
+                            : (const void *)k_vnd<V, C, Mask, false>;
+    int rc = pack ? launch_cfg_pack2<V, C>(h, fn, h->K, grid, smem)
+                  : launch_cfg<V, C>(h, fn, h->K, grid, smem);
     if (rc)
         return rc;
     const int64_t K = h->K;
@@ -1027,9 +1033,12 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     if (pack)
         k_vnd_pack2<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
                                                                   sr_out, k_max, o);
+    else if (skip)
+        k_vnd<V, C, Mask, true><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in,
+                                                                        sm_out, sr_out, k_max, o);
     else
-        k_vnd<V, C, Mask><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
-                                                                  sr_out, k_max, o);
+        k_vnd<V, C, Mask, false><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in,
+                                                                         sm_out, sr_out, k_max, o);
     CKL();
     CK(cudaEventRecord(h->ev1, st));
     k_vnd_finalize<<<1, 1024, 0, st>>>(K, o, h->summary);

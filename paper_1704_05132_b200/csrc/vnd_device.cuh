@@ -59,7 +59,11 @@ struct Slot {
     uint64_t *bar;
 };
 
-constexpr int kSlackLevels = 16;   // lm[j] = {sR setups: slack < 2^j}, lm[16] = {slack < 0}
+constexpr int kSlackLevels = 16;
+// The slack-level skip (scan_pass) shortens long delta walks, which pays
+// when the descent is latency-bound (few products per SM, GVNS tasks) and
+// costs ~7% extra instructions when it is throughput-bound; the host picks
+// per launch.   // lm[j] = {sR setups: slack < 2^j}, lm[16] = {slack < 0}
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -410,7 +414,7 @@ __device__ inline void stage_plain(const Slot<V, C> &s, const V *dem, const V *r
 // feasibility and S = sum of segment costs (warp-uniform).  Lane l owns the
 // periods [l*L, l*L+L).  Step 1 composes the (min,+) maps of its setups,
 // a warp scan gives every lane its entering X, step 2 walks the segments.
-template <typename V, typename C, typename Mask>
+template <typename V, typename C, typename Mask, bool Skip = false>
 __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
                                  const ProductCosts<C> &pc, int lane, C &S)
 {
@@ -437,7 +441,7 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
     V pa = __shfl_up_sync(FULL, A, 1), pb = __shfl_up_sync(FULL, B, 1);
     V X = lane == 0 ? V(0) : vmin<V>(pa, pb);
 
-    constexpr bool kSkip = std::is_same<Mask, MaskReg>::value;
+    constexpr bool kSkip = Skip && std::is_same<Mask, MaskReg>::value;
     C local = 0;
     bool ok = true;
     for (int u = lo; u < hi; ++u) {
@@ -647,7 +651,7 @@ __device__ inline typename PatchOf<Mask>::type patch_of(const Mask &mk, const Mo
 // takes the next unscored move, and every loop iteration advances every
 // busy lane by one segment.  Each lane still scores its moves in
 // increasing slot order, so a strict '<' keeps the earliest on ties.
-template <typename V, typename C, typename Mask>
+template <typename V, typename C, typename Mask, bool Skip = false>
 __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int T,
                                        const ProductCosts<C> &pc, C S, int nbh, int lane,
                                        C &best_out)
@@ -704,7 +708,7 @@ __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int 
         if (act) {
             int u = w.u;
             bool done = false;
-            if (std::is_same<Mask, MaskReg>::value) {
+            if (Skip && std::is_same<Mask, MaskReg>::value) {
                 // Past the move (u > b) the rows equal the base plan's and
                 // only the entering X differs (delta != 0).  A segment then
                 // costs what it costs in the base plan unless it starts at an

@@ -1,13 +1,18 @@
 #!/bin/bash
-# Build k_vnd occupancy variants and time C3/C4 with each (dev experiment).
+# Build compile-time variants of the library and time them (dev experiment).
+#   tools/variants.sh "-DRL_NO_SKIP" "-DRL_VND_MINB=5" ...
 set -e
-for minb in "$@"; do
-  out=paper_1704_05132_b200/_lib/libremlot_b200_minb$minb.so
+i=0
+for flags in "$@"; do
+  out=paper_1704_05132_b200/_lib/libremlot_b200_v$i.so
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
-     -Xcompiler -fPIC -shared -DRL_VND_MINB=$minb -o $out paper_1704_05132_b200/csrc/remlot_b200.cu &
+     -Xcompiler -fPIC -shared $flags -o $out paper_1704_05132_b200/csrc/remlot_b200.cu &
+  i=$((i+1))
 done
 wait
-for minb in "$@"; do
-  echo "== minb $minb"
-  REMLOT_B200_LIB=$PWD/paper_1704_05132_b200/_lib/libremlot_b200_minb$minb.so python tools/quick_time.py
+i=0
+for flags in "$@"; do
+  echo "== variant $i: $flags"
+  REMLOT_B200_LIB=$PWD/paper_1704_05132_b200/_lib/libremlot_b200_v$i.so python tools/quick_time.py | grep "packed=0\|T=520"
+  i=$((i+1))
 done
