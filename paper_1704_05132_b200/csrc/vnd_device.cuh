@@ -257,18 +257,20 @@ struct MaskReg {
 };
 
 struct PatchedReg {
-    uint64_t M, R, S;   // S = M | R | sentinel
+    uint64_t M, R, SR;   // SR = bit-reversed (M | R | sentinel)
     PatchedReg() = default;
     __device__ PatchedReg(const MaskReg &base, int a, int b, bool ma, bool ra, bool mb, bool rb)
     {
         const uint64_t ba = 1ull << a, bb = 1ull << b, clr = ~(ba | bb);
         M = (base.M & clr) | (ma ? ba : 0) | (mb ? bb : 0);
         R = (base.R & clr) | (ra ? ba : 0) | (rb ? bb : 0);
-        S = M | R | base.sentinel();
+        SR = __brevll(M | R | base.sentinel());
     }
     __device__ bool m(int t) const { return (M >> t) & 1; }
     __device__ bool r(int t) const { return (R >> t) & 1; }
-    __device__ int next(int x) const { return MaskReg::next_of(S, x, 0); }
+    // period t is bit 63-t of SR: shifting left by x drops periods < x and
+    // the leading one is the first setup >= x (count leading zeros)
+    __device__ int next(int x) const { return x + __clzll((long long)(SR << x)); }
 };
 
 template <typename Mask> struct PatchOf;
