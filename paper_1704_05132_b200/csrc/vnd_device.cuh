@@ -346,11 +346,10 @@ __device__ inline bool seg_cost(const V *cd, const V *cr, int T, int u, int v, b
     const V avail = cr[u + 1] - X;
     xr = r ? vmin(seg, avail) : V(0);
     const V xm = seg - xr;
-    if (xm > 0 && !m)
-        return false;
+    // computed unconditionally (no branch): callers discard c when infeasible
     c = (xr > 0 ? pc.kr : C(0)) + (xm > 0 ? pc.km : C(0)) + pc.pr * C(xr) + pc.pm * C(xm) +
         C(T - u) * (pc.hm * C(seg) - pc.hr * C(xr));
-    return true;
+    return !(xm > 0 && !m);
 }
 
 // ------------------------------------------------------------ staging
@@ -688,18 +687,15 @@ __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int 
             const MoveDesc d = slot_move(mk, nbh, w.slot, T);
             int a;
             w.nw = patch_of<V, C, Mask>(mk, d, a, w.b);
-            w.u = mk.prev(a);
-            if (w.u < 0) {
-                w.u = w.nw.next(0);
-                w.acc = 0;
-                w.X = 0;
-                act = s.cd[w.u] == 0;   // demand before the first setup: infeasible
-            } else {
-                w.acc = s.cpre[w.u];
-                w.X = s.xin[w.u];
-                act = true;
-            }
-            if (act && w.u >= T) {   // no setup at all and no demand
+            const int p = mk.prev(a);
+            const int pp = p < 0 ? 0 : p;
+            const int u0 = p < 0 ? w.nw.next(0) : p;
+            w.u = u0;
+            w.acc = p < 0 ? C(0) : s.cpre[pp];
+            w.X = p < 0 ? V(0) : s.xin[pp];
+            // no setup before the move: demand ahead of the first setup is infeasible
+            act = p >= 0 || s.cd[u0] == 0;
+            if (act && u0 >= T) {   // no setup at all and no demand: cost 0
                 act = false;
                 if (w.acc < best) {
                     best = w.acc;
@@ -718,7 +714,6 @@ __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int 
                 // changes).  Jump to the next setup in the slack-level mask
                 // that bounds that set (false positives are merely evaluated
                 // exactly) and add the base cost of the skipped segments.
-                // Written branch-free: lanes still inside the move keep q = u.
                 const bool ph2 = u > w.b;
                 const V delta = w.X - s.xin[u];
                 const int j = delta <= 1 ? 0 : 64 - __clzll((long long)(uint64_t)(delta - 1));
@@ -734,30 +729,28 @@ __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int 
                 done = q >= T;
                 u = qq;
             }
-            if (!done) {
-                const int v = w.nw.next(u + 1);
-                C c;
-                V xr;
-                if (!seg_cost<V, C>(s.cd, s.cr, T, u, v, w.nw.m(u), w.nw.r(u), w.X, pc, c, xr)) {
-                    act = false;
-                } else {
-                    w.acc += c;
-                    w.X += xr;
-                    w.u = v;
-                    done = v >= T;
-                    if (!done && v > w.b && w.X == s.xin[v]) {
-                        w.acc += S - s.cpre[v];
-                        done = true;
-                    }
-                }
-            }
-            if (done) {
-                act = false;
-                if (w.acc < best) {
-                    best = w.acc;
-                    key = w.slot;
-                }
-            }
+            // one segment of the walk, branch-free (every busy lane issues the
+            // same instructions): cost, resync test, finish, argmin update
+            const int v = w.nw.next(u + 1);
+            C c;
+            V xr;
+            const bool ok = seg_cost<V, C>(s.cd, s.cr, T, u, v, w.nw.m(u), w.nw.r(u), w.X, pc, c,
+                                           xr);
+            const int vv = v < T ? v : T - 1;
+            const V xv = s.xin[vv];
+            const C cv = s.cpre[vv];
+            const C acc = done ? w.acc : w.acc + c;
+            const V X = w.X + xr;
+            const bool sync = !done && v < T && v > w.b && X == xv;
+            const bool fin = done || v >= T || sync;
+            const C total = sync ? acc + (S - cv) : acc;
+            const bool take = (done || ok) && fin && total < best;
+            best = take ? total : best;
+            key = take ? w.slot : key;
+            act = !done && ok && !fin;
+            w.acc = acc;
+            w.X = X;
+            w.u = v;
         }
         const bool idle = !(pend | act);
         const unsigned m = __ballot_sync(FULL, idle);
