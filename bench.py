@@ -116,9 +116,16 @@ def cpu_reference(inst, sample_products, steps, warmup, threads):
                 sweeps=stats["sweeps"])
 
 
-def int32_peak(torch, ext):
-    """Measured INT32 add throughput (ops/s) of this GPU (rl microbench)."""
-    return ext.int_peak()
+def traffic_bytes(workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_vnd launch on
+    this workload from the committed ncu --set full capture (profiles/), or
+    None when no capture of the current round exists."""
+    path = os.path.join(ROOT, "profiles", f"k_vnd_{workload}_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)["bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def main():
@@ -293,7 +300,7 @@ def main():
                          "peak_source": "INT32 add microbenchmark run in this bench",
                          "ops_definition": "8*T int ops per performed neighbor evaluation "
                                            "(SURVEY.md 8(d))",
-                         "kernel_ms": vnd_kernel_ms, "traffic": None},
+                         "kernel_ms": vnd_kernel_ms, "traffic": traffic_bytes(args.workload)},
         }
         if world == 1 and not args.no_cpu_baseline:
             # bounded sample sized for ~10-20 s of CPU work on this host

@@ -318,6 +318,10 @@ struct VndOut {
 // register-mask variant runs 6 x 4 warps per SM; measured).
 template <typename V, typename C, typename Mask> struct VndMinBlocks { static constexpr int value = 1; };
 template <> struct VndMinBlocks<int32_t, int32_t, MaskReg> { static constexpr int value = 7; };
+#ifndef RL_SMEM_MINB
+#define RL_SMEM_MINB 3
+#endif
+template <> struct VndMinBlocks<int32_t, int64_t, MaskSmem> { static constexpr int value = RL_SMEM_MINB; };
 #ifdef RL_VND_MINB
 #define RL_VND_MINB_OF(V, C, M) RL_VND_MINB
 #else

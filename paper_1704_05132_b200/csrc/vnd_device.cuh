@@ -76,7 +76,7 @@ __host__ __device__ inline size_t slot_bytes(int T)
     b += align16((size_t)(T + 1) * sizeof(V));   // cd
     b += align16((size_t)(T + 1) * sizeof(V));   // cr
     b += align16((size_t)T * sizeof(V));         // xin
-    b += align16((size_t)T * sizeof(V));         // slk
+    b += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));   // slk (register-mask path only)
     b += align16((size_t)T * sizeof(C));         // cpre
     b += align16(2 * (size_t)NW * sizeof(uint32_t));
     b += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
@@ -95,7 +95,7 @@ __device__ inline Slot<V, C> carve(unsigned char *base, int T)
     s.cd = (V *)p;    p += align16((size_t)(T + 1) * sizeof(V));
     s.cr = (V *)p;    p += align16((size_t)(T + 1) * sizeof(V));
     s.xin = (V *)p;   p += align16((size_t)T * sizeof(V));
-    s.slk = (V *)p;   p += align16((size_t)T * sizeof(V));
+    s.slk = (V *)p;   p += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));
     s.cpre = (C *)p;  p += align16((size_t)T * sizeof(C));
     s.bm = (uint32_t *)p;
     s.br = s.bm + NW; p += align16(2 * (size_t)NW * sizeof(uint32_t));
