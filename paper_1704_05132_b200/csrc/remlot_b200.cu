@@ -1011,7 +1011,11 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     const bool pack = std::is_same<Mask, MaskReg>::value && h->pack2;
     // skip pays when the launch is latency-bound: fewer products than ~2
     // waves of resident warps (C2, GVNS) -- measured, DESIGN.md section 5
+#ifdef RL_SKIP_ALWAYS
+    const bool skip = std::is_same<Mask, MaskReg>::value;
+#else
     const bool skip = std::is_same<Mask, MaskReg>::value && h->K < (int64_t)h->sms * 64;
+#endif
     const void *fn = pack ? (const void *)k_vnd_pack2<V, C>
                      : skip ? (const void *)k_vnd<V, C, Mask, true>
                             : (const void *)k_vnd<V, C, Mask, false>;

@@ -17,4 +17,5 @@ for K, T in ((1000, 52), (100000, 52), (10000, 520)):
             m, r, tr, st = dev.vnd(sm, sr)
             t1 = time.perf_counter()
             print(f"K={K} T={T} packed={packed} wall {1e3 * (t1 - t0):.1f} ms "
-                  f"kernel {st['kernel_ns'] / 1e6:.2f} ms cost {st['cost']}", flush=True)
+                  f"kernel {st['kernel_ns'] / 1e6:.2f} ms cost {st['cost']} scored {st.get('evals_scored')} "
+                  f"of {st['evals']}", flush=True)
