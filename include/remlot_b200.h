@@ -49,6 +49,12 @@ int rl_instance_update(rl_instance *h, const int64_t *demand, const int64_t *ret
                        const int64_t *hold_m, const int64_t *hold_r,
                        const int64_t *unit_m, const int64_t *unit_r);
 void rl_instance_destroy(rl_instance *h);
+/* _kernels.oracle_product / oracle.enumerate_optimal (_kernels.py:347-371,
+ * oracle.py:19-44): per product the minimum cost over all 2^(2T) setup
+ * patterns (lowest (m, r) mask pair on ties) and that pattern; T <= 10
+ * (larger T -> RL_EINVAL like the reference's ValueError). */
+int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uint8_t *sr);
+
 /* Kernel variant of rl_vnd for T <= 64: packed = 1 runs two products per
  * warp in lockstep sweeps, 0 (default) one product per warp.  Results are
  * identical; the switch exists for A/B measurement and tests. */

@@ -23,7 +23,7 @@ EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_instance_set_variant",
            "rl_instance_info", "rl_product_costs", "rl_scan_products", "rl_apply_scan",
            "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect",
-           "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
+           "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_oracle_optimal", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
            "rl_gvns_round", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
            "rl_rng_probe", "rl_launch_count",
            "rl_last_error")
@@ -65,6 +65,7 @@ def load():
         "rl_initial_solution_device": (I, [P, P, P, P]),
         "rl_decode": (I, [P] + [P] * 7),
         "rl_int_peak": (I, [P]),
+        "rl_oracle_optimal": (I, [P, P, P, P]),
         "rl_gvns_begin": (I, [P, I, I64, I, I, ctypes.c_uint64, P, P, P]),
         "rl_gvns_candidate": (I, [P, P, P]),
         "rl_gvns_import": (I, [P, P, I64]),
@@ -244,6 +245,15 @@ class DeviceInstance:
         return sm, sr, dict(inc_cost=int(info[0]), strength=int(info[1]),
                             best_cost=int(info[2]), best_worker=int(info[3]),
                             accepted=int(info[4]), fallbacks=int(info[5]))
+
+    def oracle_optimal(self):
+        """Exhaustive per-product optimum (T <= 10): (costs, sm, sr)."""
+        cost = np.zeros(self.K, np.int64)
+        sm = np.empty((self.K, self.T), np.bool_)
+        sr = np.empty((self.K, self.T), np.bool_)
+        check(load().rl_oracle_optimal(self.h, ptr(cost), ptr(sm.view(np.uint8)),
+                                       ptr(sr.view(np.uint8))), "rl_oracle_optimal")
+        return cost, sm, sr
 
     def initial_solution(self):
         sm = np.empty((self.K, self.T), np.bool_)

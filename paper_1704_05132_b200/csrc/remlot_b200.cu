@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 #include <type_traits>
 
 #include "../../include/remlot_b200.h"
@@ -599,6 +600,7 @@ struct rl_instance {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timing = false;
     struct GvnsState *gv = nullptr;        // device GVNS state (gvns_impl.cuh)
+    double cost_bound = 0.0;               // upper bound of any plan's cost (upload)
     bool pack2 = false;                    // T <= 63: two products per warp (vnd_packed.cuh;
                                            // measured slower, kept for A/B)
 };
@@ -648,6 +650,7 @@ static int upload(rl_instance *h, const int64_t *demand, const int64_t *returns,
         return fail(RL_ERANGE,
                     "instance too large for exact int64 costs (max sum D+R %.3g, cost bound %.3g)",
                     sdr, B);
+    h->cost_bound = B;
     const int vbytes = sdr < std::ldexp(1.0, 28) ? 4 : 8;
     const int cbytes = (vbytes == 4 && B < std::ldexp(1.0, 30)) ? 4 : 8;
     if (h->dem && h->vbytes == 4 && vbytes != 4) {
@@ -1221,6 +1224,123 @@ extern "C" int rl_decode(rl_instance *h, const uint8_t *sm, const uint8_t *sr, i
             e = cudaStreamSynchronize(h->stream);
         if (e != cudaSuccess)
             rc = fail(RL_ECUDA, "rl_decode: %s", cudaGetErrorString(e));
+    } while (0);
+    cudaFree(d);
+    return rc;
+}
+
+// _kernels.oracle_product (_kernels.py:347-371) / oracle.enumerate_optimal
+// (oracle.py:19-44): every (m mask, r mask) pair of a product, T <= 10, one
+// thread per pattern p = m * 2^T + r; the per-product minimum of the packed
+// key (cost << 20 | p) keeps the lowest (m, r) pair on ties like the
+// reference's strict '<' over its nested loops.  Cost by the reference's
+// per-period recurrence in int64.
+__global__ void k_oracle(int64_t K, int T, const int64_t *dem, const int64_t *ret,
+                         const int64_t *c6, unsigned long long *best)
+{
+    const int64_t k = blockIdx.y;
+    const uint32_t npat = 1u << (2 * T);
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long key = ~0ull;
+    if (p < npat) {
+        const uint32_t mm = p >> T, mr = p & ((1u << T) - 1);
+        const int64_t *d = dem + k * T, *r = ret + k * T;
+        const int64_t km = c6[k], kr = c6[K + k], hm = c6[2 * K + k], hr = c6[3 * K + k],
+                      pm = c6[4 * K + k], pr = c6[5 * K + k];
+        int64_t cost = 0, rec = 0, stock = 0;
+        bool ok = true;
+        int t = 0;
+        for (; t < T && !(((mm | mr) >> t) & 1); ++t) {
+            ok &= d[t] <= 0;
+            rec += r[t];
+            cost += hr * rec;
+        }
+        while (ok && t < T) {
+            const int u = t;
+            int v = u + 1;
+            while (v < T && !(((mm | mr) >> v) & 1))
+                ++v;
+            int64_t need = 0;
+            for (int i = u; i < v; ++i)
+                need += d[i];
+            const int64_t have = rec + r[u];
+            const int64_t xr = ((mr >> u) & 1) ? (need < have ? need : have) : 0;
+            const int64_t xm = need - xr;
+            if (xm > 0 && !((mm >> u) & 1)) {
+                ok = false;
+                break;
+            }
+            cost += (xr > 0 ? kr : 0) + (xm > 0 ? km : 0) + pr * xr + pm * xm;
+            for (int i = u; i < v; ++i) {
+                if (i == u) {
+                    stock += xm + xr;
+                    rec += r[i] - xr;
+                } else {
+                    rec += r[i];
+                }
+                stock -= d[i];
+                cost += hm * stock + hr * rec;
+            }
+            t = v;
+        }
+        if (ok)
+            key = ((unsigned long long)cost << 20) | p;
+    }
+    for (int off = 16; off; off >>= 1)
+        key = min(key, (unsigned long long)__shfl_xor_sync(FULL, key, off));
+    if ((threadIdx.x & 31) == 0 && key != ~0ull)
+        atomicMin(&best[k], key);
+}
+
+extern "C" int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uint8_t *sr)
+{
+    (void)cudaGetLastError();
+    if (!h || !cost || !sm || !sr)
+        return fail(RL_EINVAL, "rl_oracle_optimal: bad arguments");
+    if (h->T > 10)
+        return fail(RL_EINVAL,
+                    "exhaustive enumeration needs periods <= 10 (2^(2*%d) patterns per product "
+                    "is intractable)", h->T);
+    if (!(h->cost_bound < std::ldexp(1.0, 43)))
+        return fail(RL_ERANGE, "rl_oracle_optimal: costs up to %.3g do not fit the packed "
+                    "(cost, pattern) key", h->cost_bound);
+    CK(cudaSetDevice(h->device));
+    const int64_t K = h->K;
+    const int T = h->T;
+    unsigned long long *d = nullptr;
+    CK(cudaMalloc(&d, K * 8));
+    int rc = 0;
+    std::vector<unsigned long long> hk((size_t)K);
+    do {
+        cudaError_t e = cudaMemsetAsync(d, 0xff, K * 8, h->stream);
+        if (e == cudaSuccess) {
+            const uint32_t npat = 1u << (2 * T);
+            dim3 grid((npat + 255) / 256, (unsigned)K);
+            k_oracle<<<grid, 256, 0, h->stream>>>(K, T, h->dem64, h->ret64, h->cost6, d);
+            ++h->launches;
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(hk.data(), d, K * 8, cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess)
+            e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) {
+            rc = fail(RL_ECUDA, "rl_oracle_optimal: %s", cudaGetErrorString(e));
+            break;
+        }
+        for (int64_t k = 0; k < K; ++k) {
+            const unsigned long long key = hk[(size_t)k];
+            if (key == ~0ull) {   // unreachable: all-manufacturing is always feasible
+                cost[k] = RL_INFEASIBLE;
+                continue;
+            }
+            cost[k] = (int64_t)(key >> 20);
+            const uint32_t p = (uint32_t)(key & 0xFFFFF);
+            for (int t = 0; t < T; ++t) {
+                sm[k * T + t] = ((p >> T) >> t) & 1;
+                sr[k * T + t] = ((p & ((1u << T) - 1)) >> t) & 1;
+            }
+        }
     } while (0);
     cudaFree(d);
     return rc;

@@ -388,8 +388,26 @@ def gen_gvns_k1000():
         json.dump(out, f, indent=1)
 
 
+def gen_oracle_optimal():
+    """enumerate_optimal (reference oracle.py:19-44) on small instances."""
+    from remlot import enumerate_optimal
+    out = []
+    for seed, K, T, dmax in ((0, 3, 5, 9), (1, 2, 6, 9), (2, 4, 4, 5), (3, 1, 8, 9),
+                             (4, 2, 10, 9), (5, 2, 1, 3), (6, 3, 3, 0)):
+        inst = random_instance(seed, products=K, periods=T, demand_max=dmax,
+                               setup_cost_range=(200, 8000), holding_cost_range=(100, 500))
+        cost, plan = enumerate_optimal(inst)
+        out.append(dict(seed=seed, products=K, periods=T, demand_max=dmax, cost=int(cost),
+                        sm=plan.setup_m.astype(int).tolist(), sr=plan.setup_r.astype(int).tolist()))
+    with open(os.path.join(HERE, "oracle_optimal.json"), "w") as f:
+        json.dump(out, f)
+
+
 if __name__ == "__main__":
     _kernels.warm_up()
+    if "--oracle-only" in sys.argv:
+        gen_oracle_optimal()
+        sys.exit(0)
     gen_instances()
     gen_rng()
     gen_small_cases()
@@ -397,5 +415,7 @@ if __name__ == "__main__":
     gen_k1000()
     gen_gvns_small()
     gen_gvns_k1000()
+    gen_oracle_optimal()
     if "--big" in sys.argv:
         gen_big()
+

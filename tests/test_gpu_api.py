@@ -290,21 +290,10 @@ def test_gvns_determinism_and_counts():
 
 
 def test_gvns_reaches_oracle_optimum():
+    from paper_1704_05132_b200 import enumerate_optimal
     inst = random_instance(7, products=2, periods=5, demand_max=9)
     res = gvns(inst, SolverConfig(t_max=1e9, max_rounds=300, workers=2, seed=4, k_max=3))
-    best = 0
-    for k in range(2):   # exhaustive per-product optimum (the reference oracle.py)
-        b = INFEASIBLE
-        for mm in range(32):
-            for mr in range(32):
-                sm = [(mm >> t) & 1 for t in range(5)]
-                sr = [(mr >> t) & 1 for t in range(5)]
-                b = min(b, oracle.row_cost(sm, sr, inst.demand[k], inst.returns[k],
-                                           int(inst.setup_cost_m[k]), int(inst.setup_cost_r[k]),
-                                           int(inst.holding_cost_m[k]),
-                                           int(inst.holding_cost_r[k])))
-        best += b
-    assert res.cost == best
+    assert res.cost == enumerate_optimal(inst)[0]
 
 
 def test_solve_scheme_dispatch():
@@ -323,3 +312,35 @@ def test_solve_scheme_dispatch():
                 dict(t_max=1, scheme="bogus"), dict(t_max=1, vnd_mode="gpu")):
         with pytest.raises(ValueError):
             SolverConfig(**bad)
+
+
+# ---- oracle (reference oracle.py / test_oracle.py) ------------------------
+
+def test_enumerate_optimal_matches_reference_goldens():
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_1704_05132_b200 import enumerate_optimal
+    with open(os.path.join(GOLDEN, "oracle_optimal.json")) as f:
+        gold = json.load(f)
+    for g in gold:
+        inst = generate_instance(GeneratorConfig(
+            products=g["products"], periods=g["periods"], demand_max=g["demand_max"],
+            return_ratio=0.6, setup_cost_range=(200, 8000), holding_cost_range=(100, 500),
+            seed=g["seed"]))
+        cost, plan = enumerate_optimal(inst)
+        assert cost == g["cost"]
+        assert plan.setup_m.astype(int).tolist() == g["sm"]
+        assert plan.setup_r.astype(int).tolist() == g["sr"]
+        assert evaluate(inst, plan) == cost
+
+
+def test_enumerate_optimal_bounds_heuristics_and_refuses_long_horizons():
+    from paper_1704_05132_b200 import enumerate_optimal
+    for seed in range(5):
+        inst = random_instance(100 + seed, products=3, periods=6)
+        opt, plan = enumerate_optimal(inst)
+        assert vnd(inst, initial_solution(inst))[1] >= opt
+        assert evaluate(inst, plan) == opt
+    with pytest.raises(ValueError):
+        enumerate_optimal(random_instance(1, products=1, periods=11))
