@@ -53,6 +53,7 @@ template <typename V, typename C>
 struct Slot {
     V *stage, *cd, *cr, *xin, *slk;
     C *cpre;
+    int16_t *nx, *pv;   // T > 63: next setup >= t / last setup < t of the base plan
     uint32_t *bm, *br;
     uint16_t *mv;
     uint64_t *lm;
@@ -78,6 +79,7 @@ __host__ __device__ inline size_t slot_bytes(int T)
     b += align16((size_t)T * sizeof(V));         // xin
     b += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));   // slk (register-mask path only)
     b += align16((size_t)T * sizeof(C));         // cpre
+    b += 2 * align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));   // nx, pv
     b += align16(2 * (size_t)NW * sizeof(uint32_t));
     b += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
     b += align16((kSlackLevels + 1) * 8);        // lm
@@ -97,6 +99,8 @@ __device__ inline Slot<V, C> carve(unsigned char *base, int T)
     s.xin = (V *)p;   p += align16((size_t)T * sizeof(V));
     s.slk = (V *)p;   p += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));
     s.cpre = (C *)p;  p += align16((size_t)T * sizeof(C));
+    s.nx = (int16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));
+    s.pv = (int16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));
     s.bm = (uint32_t *)p;
     s.br = s.bm + NW; p += align16(2 * (size_t)NW * sizeof(uint32_t));
     s.mv = (uint16_t *)p; p += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
@@ -160,41 +164,20 @@ __device__ inline V vmin(V a, V b) { return a < b ? a : b; }
 
 __device__ inline bool wbit(const uint32_t *w, int t) { return (w[t >> 5] >> (t & 31)) & 1u; }
 
-// Setup rows held in shared memory words (any T).
+// Setup rows held in shared memory words (T > 63).  Next/previous-setup
+// queries read per-period tables (nx, pv) that base_pass rebuilds whenever
+// the rows change, so they are one shared-memory load each.
 struct MaskSmem {
     uint32_t *bm, *br;
+    int16_t *nx, *pv;
     int T;
     __device__ bool m(int t) const { return wbit(bm, t); }
     __device__ bool r(int t) const { return wbit(br, t); }
-    // smallest setup period >= x (T if none)
-    __device__ int next(int x) const
-    {
-        if (x >= T)
-            return T;
-        const int NW = (T + 31) >> 5;
-        int i = x >> 5;
-        uint32_t w = (bm[i] | br[i]) & (FULL << (x & 31));
-        while (!w) {
-            if (++i >= NW)
-                return T;
-            w = bm[i] | br[i];
-        }
-        return (i << 5) + __ffs(w) - 1;
-    }
-    // largest setup period < x (-1 if none)
-    __device__ int prev(int x) const
-    {
-        if (x <= 0)
-            return -1;
-        int i = (x - 1) >> 5;
-        uint32_t w = (bm[i] | br[i]) & (FULL >> (31 - ((x - 1) & 31)));
-        while (!w) {
-            if (--i < 0)
-                return -1;
-            w = bm[i] | br[i];
-        }
-        return (i << 5) + 31 - __clz(w);
-    }
+    __device__ bool setup(int t) const { return wbit(bm, t) | wbit(br, t); }
+    // smallest setup period >= x (T if none); needs fresh tables
+    __device__ int next(int x) const { return x >= T ? T : nx[x]; }
+    // largest setup period < x (-1 if none); needs fresh tables
+    __device__ int prev(int x) const { return x <= 0 ? -1 : pv[x]; }
     __device__ void set(int t, bool mv, bool rv, int lane)
     {
         if (lane == 0) {
@@ -204,7 +187,49 @@ struct MaskSmem {
         }
     }
     __device__ void sync() const { __syncwarp(); }
-    __device__ uint64_t R_mask() const { return 0; }   // unused (no skip for T > 64)
+    __device__ uint64_t R_mask() const { return 0; }   // unused (no skip for T > 63)
+    // rebuild nx/pv from the bit rows (lane chunks + warp min/max scans)
+    __device__ void build_tables(int lane) const
+    {
+        const int L = (T + 31) >> 5;
+        const int lo = lane * L, hi = min(lo + L, T);
+        int first = T, last = -1;
+        for (int t = lo; t < hi; ++t)
+            if (setup(t)) {
+                first = min(first, t);
+                last = t;
+            }
+        int sf = first, pl = last;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_down_sync(FULL, sf, off), q = __shfl_up_sync(FULL, pl, off);
+            if (lane + off < 32)
+                sf = min(sf, o);
+            if (lane >= off)
+                pl = max(pl, q);
+        }
+        int run = __shfl_down_sync(FULL, sf, 1);
+        if (lane == 31)
+            run = T;
+        for (int t = hi - 1; t >= lo; --t) {
+            if (setup(t))
+                run = t;
+            nx[t] = (int16_t)run;
+        }
+        run = __shfl_up_sync(FULL, pl, 1);
+        if (lane == 0)
+            run = -1;
+        for (int t = lo; t < hi; ++t) {
+            pv[t] = (int16_t)run;
+            if (setup(t))
+                run = t;
+        }
+        if (lane == 31) {
+            nx[T] = (int16_t)T;
+            pv[T] = (int16_t)pl;
+        }
+        __syncwarp();
+    }
 };
 
 // The rows of a candidate move: base rows with periods a <= b rewritten.
@@ -307,7 +332,7 @@ __device__ inline MaskSmem load_rows(const Slot<V, C> &s, MaskSmem, const uint8_
         }
     }
     __syncwarp();
-    return MaskSmem{s.bm, s.br, T};
+    return MaskSmem{s.bm, s.br, s.nx, s.pv, T};
 }
 
 template <typename V, typename C>
@@ -419,6 +444,8 @@ template <typename V, typename C, typename Mask, bool Skip = false>
 __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
                                  const ProductCosts<C> &pc, int lane, C &S)
 {
+    if constexpr (std::is_same<Mask, MaskSmem>::value)
+        mk.build_tables(lane);
     const int L = (T + 31) >> 5;
     const int lo = lane * L, hi = min(lo + L, T);
     const V INF = VInf<V>::value;
