@@ -183,9 +183,18 @@ def main():
     from paper_1704_05132_b200 import _native
     from paper_1704_05132_b200 import devbench, sharded
 
-    torch.cuda.set_device(local_rank)
+    # RL_BENCH_BACKEND=gloo runs the multi-rank plumbing with several ranks
+    # on one GPU (test only: NCCL refuses two ranks per device); collectives
+    # then go through host tensors.
+    backend = os.environ.get("RL_BENCH_BACKEND", "nccl")
+    dev_idx = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_idx)
+    coll = "cuda" if backend == "nccl" else "cpu"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
     K, T = wl["products"], wl["periods"]
     inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=0))
     from paper_1704_05132_b200.sharded import shard_bounds
@@ -225,7 +234,7 @@ def main():
     torch.cuda.synchronize()
     st = collect()
     # ---- timed region (device): per-step CUDA events, L2 flushed between steps
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_idx)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -251,9 +260,9 @@ def main():
     trace, stats = collect()
     # totals across ranks: time = max over ranks, work = the combined lockstep
     # counts (sharded.combine rebuilds the global trace and evaluation count)
-    tmax = torch.tensor([my_ms, float(np.mean(kernel_ms))], dtype=torch.float64, device="cuda")
+    tmax = torch.tensor([my_ms, float(np.mean(kernel_ms))], dtype=torch.float64, device=coll)
     if world > 1:
-        g_trace, totals = sharded.combine(trace, stats, device="cuda")
+        g_trace, totals = sharded.combine(trace, stats, device=coll)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     else:
         g_trace, totals = trace, dict(evals_reference=stats["evals_reference"],
@@ -265,7 +274,8 @@ def main():
     ms_per_step = total_ms / args.steps
 
     # ---- e2e through the C ABI with pinned host buffers
-    e2e_ms, h2d, d2h = devbench.e2e_steps(torch, _native, dev, shard, args.steps, world, dist)
+    e2e_ms, h2d, d2h = devbench.e2e_steps(torch, _native, dev, shard, args.steps, world, dist,
+                                          coll)
 
     line = None
     if rank == 0:
@@ -314,9 +324,10 @@ def main():
                           f"({r['seconds_per_step']:.2f} s)"}
         if world == 1 and not args.no_extra:
             line["other_configs"] = devbench.other_configs(torch)
-        if args.workload == "c3" and world == 1:
+        if args.workload == "c3":
             line["parity"] = {"final_cost": final_cost, "reference_final_cost": 449100704810,
-                              "bit_exact": final_cost == 449100704810}
+                              "bit_exact": final_cost == 449100704810,
+                              "evals_reference_golden": ref_evals == 878715402}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -529,45 +529,6 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
 
 // ------------------------------------------------------- move scoring
 
-// Score a candidate whose rows are `nw` (base rows rewritten at a <= b):
-// re-walk from the last setup before a with the base pass's state, until
-// past b with X equal to the base plan's, then add the base suffix.
-// Returns false if the candidate is infeasible, else Snew.
-template <typename V, typename C, typename Mask, typename Patched>
-__device__ inline bool score_move(const Slot<V, C> &s, const Mask &mk, const Patched &nw, int a,
-                                  int b, int T, const ProductCosts<C> &pc, C S, C &Snew)
-{
-    int u = mk.prev(a);
-    C acc;
-    V X;
-    if (u < 0) {
-        u = nw.next(0);
-        if (s.cd[u] > 0)
-            return false;
-        acc = 0;
-        X = 0;
-    } else {
-        acc = s.cpre[u];
-        X = s.xin[u];
-    }
-    while (u < T) {
-        const int v = nw.next(u + 1);
-        C c;
-        V xr;
-        if (!seg_cost<V, C>(s.cd, s.cr, T, u, v, nw.m(u), nw.r(u), X, pc, c, xr))
-            return false;
-        acc += c;
-        X += xr;
-        u = v;
-        if (u > b && u < T && X == s.xin[u]) {
-            acc += S - s.cpre[u];
-            break;
-        }
-    }
-    Snew = acc;
-    return true;
-}
-
 // A move in reference form (list_moves, _kernels.py:188-258): period p0
 // (and p1 >= 0 for shifts) with the new bits of both rows there.
 struct MoveDesc {
@@ -621,29 +582,16 @@ __device__ inline MoveDesc slot_move(const Mask &mk, int nbh, int slot, int T)
     return d;
 }
 
-template <typename V, typename C, typename Mask>
-__device__ inline bool score_desc(const Slot<V, C> &s, const Mask &mk, const MoveDesc &d, int T,
-                                  const ProductCosts<C> &pc, C S, C &c)
-{
-    if (d.p1 < 0) {
-        const auto nw = PatchOf<Mask>::make(mk, d.p0, d.p0, d.m0, d.r0, d.m0, d.r0);
-        return score_move(s, mk, nw, d.p0, d.p0, T, pc, S, c);
-    }
-    if (d.p1 < d.p0) {
-        const auto nw = PatchOf<Mask>::make(mk, d.p1, d.p0, d.m1, d.r1, d.m0, d.r0);
-        return score_move(s, mk, nw, d.p1, d.p0, T, pc, S, c);
-    }
-    const auto nw = PatchOf<Mask>::make(mk, d.p0, d.p1, d.m0, d.r0, d.m1, d.r1);
-    return score_move(s, mk, nw, d.p0, d.p1, T, pc, S, c);
-}
-
 struct PassResult {
     bool improved;
     int slot;     // winning canonical slot
     int n_moves;  // candidates scored (list_moves count)
 };
 
-// Per-lane state of one delta walk (score_move unrolled into steps).
+// Per-lane state of one delta walk.  A move rewrites periods a <= b; its
+// cost is the base plan's prefix up to the last setup before a (cpre, xin),
+// the re-walked segments, and -- once past b the walk's X equals the base
+// plan's X at a setup -- the base plan's suffix.
 template <typename V, typename C, typename Mask>
 struct Walk {
     typename PatchOf<Mask>::type nw;

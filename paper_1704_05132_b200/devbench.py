@@ -22,7 +22,7 @@ def _pinned(torch, a):
     return t, arr
 
 
-def e2e_steps(torch, _native, dev, shard, steps, world, dist):
+def e2e_steps(torch, _native, dev, shard, steps, world, dist, coll="cuda"):
     """Time `steps` end-to-end descents through the C ABI with pinned host
     buffers: each step uploads the instance (rl_instance_update) and the
     start plan, runs the VND (rl_vnd) and reads back the final plan, trace
@@ -63,8 +63,8 @@ def e2e_steps(torch, _native, dev, shard, steps, world, dist):
     ms = (time.perf_counter() - t0) * 1e3
     h2d = sum(a.nbytes for a in arrays) + sm.nbytes + sr.nbytes
     d2h = om.nbytes + orr.nbytes + int(nt[0]) * 8 + st.nbytes + 24
-    tot = torch.tensor([ms, 0.0], dtype=torch.float64, device="cuda")
-    byt = torch.tensor([h2d, d2h], dtype=torch.int64, device="cuda")
+    tot = torch.tensor([ms, 0.0], dtype=torch.float64, device=coll)
+    byt = torch.tensor([h2d, d2h], dtype=torch.int64, device=coll)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         dist.all_reduce(byt, op=dist.ReduceOp.SUM)
