@@ -81,14 +81,20 @@ __device__ inline bool row_feasible(const V *d, const V *r, int T, BitM bm, BitR
     return true;
 }
 
+// One warp per worker: lane 0 runs the (inherently sequential) numpy-exact
+// draw and the flips; the other lanes pull the touched products' rows
+// (incumbent bits, demand, returns) into L1 with coalesced loads first, so
+// lane 0's sequential feasibility walk hits the cache instead of DRAM/L2.
 template <typename V>
 __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
 {
-    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (w >= g.W)
         return;
     Philox rng;
-    rng.seed(g.seed, (uint64_t)round, (uint64_t)(g.w0 + w));
+    if (lane == 0)
+        rng.seed(g.seed, (uint64_t)round, (uint64_t)(g.w0 + w));
     const int64_t strength = g.scal[GV_STRENGTH];
     const int64_t k_eff = strength < g.pop ? strength : g.pop;   // gvns.py:113
     int64_t *P = g.pos + (int64_t)w * g.kcap;
@@ -96,49 +102,77 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
     uint32_t *tw = g.tw + (int64_t)w * g.tcap * 2 * g.NW;
     const int T = g.T, NW = g.NW;
     for (int attempt = 0; attempt < 50; ++attempt) {   // _SHAKE_REDRAWS (gvns.py:29, :114)
-        if (choice_uses_tail_shuffle(g.pop, k_eff))
-            choice_tail(rng, g.pop, k_eff, P, g.tailidx + (int64_t)w * g.pop);
-        else
-            choice_floyd(rng, g.pop, k_eff, P, g.table + (int64_t)w * g.tsize);
         int n = 0;
-        for (int64_t i = 0; i < k_eff; ++i) {   // _flip_flat (gvns.py:93-98)
-            const int64_t p = P[i];
-            const int mat = p < g.KT ? 0 : 1;
-            const int64_t rem = p % g.KT, k = rem / T;
-            const int t = (int)(rem % T);
-            int j = 0;
-            while (j < n && tp[j] != k)
-                ++j;
-            if (j == n) {
-                tp[n++] = k;
-                uint32_t *row = tw + (int64_t)j * 2 * NW;
-                for (int q = 0; q < 2 * NW; ++q)
-                    row[q] = 0;
-                const uint8_t *im = g.inc + k * T, *ir = g.inc + g.KT + k * T;
-                for (int q = 0; q < T; ++q) {
-                    row[q >> 5] |= (uint32_t)im[q] << (q & 31);
-                    row[NW + (q >> 5)] |= (uint32_t)ir[q] << (q & 31);
+        if (lane == 0) {
+            if (choice_uses_tail_shuffle(g.pop, k_eff))
+                choice_tail(rng, g.pop, k_eff, P, g.tailidx + (int64_t)w * g.pop);
+            else
+                choice_floyd(rng, g.pop, k_eff, P, g.table + (int64_t)w * g.tsize);
+            for (int64_t i = 0; i < k_eff; ++i) {   // distinct touched products
+                const int64_t k = (P[i] % g.KT) / T;
+                int j = 0;
+                while (j < n && tp[j] != k)
+                    ++j;
+                if (j == n)
+                    tp[n++] = k;
+            }
+        }
+        n = __shfl_sync(FULL, n, 0);
+        __syncwarp();
+        // rows of the touched products: incumbent bits by ballot, then flips
+        for (int j = 0; j < n; ++j) {
+            const int64_t k = tp[j];
+            const uint8_t *im = g.inc + k * T, *ir = g.inc + g.KT + k * T;
+            uint32_t *row = tw + (int64_t)j * 2 * NW;
+            for (int base = 0; base < T; base += 32) {
+                const int t = base + lane;
+                const uint32_t wm = __ballot_sync(FULL, t < T && im[t]);
+                const uint32_t wr = __ballot_sync(FULL, t < T && ir[t]);
+                if (lane == 0) {
+                    row[base >> 5] = wm;
+                    row[NW + (base >> 5)] = wr;
                 }
             }
-            tw[(int64_t)j * 2 * NW + mat * NW + (t >> 5)] ^= 1u << (t & 31);
+            for (int t = lane; t < T; t += 32) {   // warm L1 for lane 0's walk
+                (void)__ldg(in.dem + k * T + t);
+                (void)__ldg(in.ret + k * T + t);
+            }
         }
+        __syncwarp();
         bool ok = true;
-        for (int j = 0; j < n && ok; ++j) {
-            const uint32_t *row = tw + (int64_t)j * 2 * NW;
-            const int64_t k = tp[j];
-            ok = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
-                                 [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
-                                 [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
+        if (lane == 0) {
+            for (int64_t i = 0; i < k_eff; ++i) {   // _flip_flat (gvns.py:93-98)
+                const int64_t p = P[i];
+                const int mat = p < g.KT ? 0 : 1;
+                const int64_t rem = p % g.KT, k = rem / T;
+                const int t = (int)(rem % T);
+                int j = 0;
+                while (tp[j] != k)
+                    ++j;
+                tw[(int64_t)j * 2 * NW + mat * NW + (t >> 5)] ^= 1u << (t & 31);
+            }
+            for (int j = 0; j < n && ok; ++j) {
+                const uint32_t *row = tw + (int64_t)j * 2 * NW;
+                const int64_t k = tp[j];
+                ok = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
+                                     [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
+                                     [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
+            }
         }
+        ok = __shfl_sync(FULL, (int)ok, 0);
         if (ok) {
-            g.tn[w] = n;
-            g.fb[w] = 0;
+            if (lane == 0) {
+                g.tn[w] = n;
+                g.fb[w] = 0;
+            }
             return;
         }
     }
-    g.tn[w] = 0;
-    g.fb[w] = 1;
-    g.rng[w] = rng.st;
+    if (lane == 0) {
+        g.tn[w] = 0;
+        g.fb[w] = 1;
+        g.rng[w] = rng.st;
+    }
 }
 
 // gvns.py:124-137: flip the positions where the incumbent differs from the
@@ -447,7 +481,7 @@ static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round)
     const int W = gs->a.W;
     CK(cudaMemsetAsync(&gs->a.scal[GV_FB_COUNT], 0, 2 * sizeof(int64_t), h->stream));
     CK(cudaMemsetAsync(&gs->a.scal[GV_FBCOST0], 0, gs->a.fb_slots * sizeof(int64_t), h->stream));
-    k_shake<V><<<(W + 63) / 64, 64, 0, h->stream>>>(view<V>(h), gs->a, round);
+    k_shake<V><<<(W + 3) / 4, 128, 0, h->stream>>>(view<V>(h), gs->a, round);
     CKL();
     k_shake_fallback<V><<<(W + 63) / 64, 64, 0, h->stream>>>(view<V>(h), gs->a);
     CKL();
