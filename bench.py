@@ -289,7 +289,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step,
             "time_to_local_opt_ms": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "int32/int64 (exact integer cents)",
+            "dtype": "int32" if dev.info["cost_bytes"] == 4 else "int64",
             "data": "synthetic (reference generator model.py:115-153, seed 0)",
             "config": {"workload": wl["name"], "products": K, "periods": T, "k_max": 4,
                        "parallelism": f"product-shard x{world}",

@@ -55,9 +55,10 @@ void rl_instance_destroy(rl_instance *h);
  * (larger T -> RL_EINVAL like the reference's ValueError). */
 int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uint8_t *sr);
 
-/* Kernel variant of rl_vnd for T <= 64: packed = 1 runs two products per
- * warp in lockstep sweeps, 0 (default) one product per warp.  Results are
- * identical; the switch exists for A/B measurement and tests. */
+/* Kernel variants of rl_vnd (results are identical; for A/B measurement and
+ * tests).  Bit 0: T <= 63 runs two products per warp in lockstep sweeps
+ * (default off).  Bit 1: T > 63 never uses one CTA per product (by default
+ * a CTA per product is used when K <= 2 x SMs, a warp per product above). */
 int rl_instance_set_variant(rl_instance *h, int packed);
 /* info[0..5] = K, T, bytes per period value (4|8), bytes per cost (4|8),
  * SM count, warps per CTA of the resident VND kernel. */

@@ -129,7 +129,8 @@ class DeviceInstance:
             self.h = None
 
     def set_variant(self, packed):
-        """T <= 64: 1 = two products per warp, 0 = one per warp (default)."""
+        """Kernel variant bits (identical results): 1 = two products per warp
+        for T <= 63, 2 = warp (not CTA) per product for T > 63; 0 = default."""
         check(load().rl_instance_set_variant(self.h, int(packed)), "rl_instance_set_variant")
 
     @property

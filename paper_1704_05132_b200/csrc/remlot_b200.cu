@@ -26,6 +26,8 @@
 
 using namespace rl;
 
+constexpr int kWarpsPerCta = 4;
+
 static thread_local std::string g_err;
 
 static int fail(int code, const char *fmt, ...)
@@ -379,6 +381,145 @@ __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstVie
     }
 }
 
+// Long horizons (T > 63): one CTA of kWarpsPerCta warps per product.  A pass
+// has ~2T moves, so the walks are split over all warps (move i goes to warp
+// i mod 4; each lane still sees its moves in slot order) and the per-warp
+// minima are combined in shared memory.  Warp 0 does the inherently
+// per-product steps (staging, base pass, enumeration, apply) -- the same
+// device functions as k_vnd, so results are identical.
+template <typename V, typename C>
+__global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *sm_in,
+                                                 const uint8_t *sr_in, uint8_t *sm_out,
+                                                 uint8_t *sr_out, int k_max, VndOut o)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ C part_best[kWarpsPerCta];
+    __shared__ int part_key[kWarpsPerCta];
+    __shared__ int64_t sh_k, sh_next;
+    __shared__ C sh_S, sh_best;
+    __shared__ int sh_n, sh_key, sh_feas;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = in.T;
+    const Slot<V, C> s = carve<V, C>(smem, T);
+    const MaskSmem mk{s.bm, s.br, s.nx, s.pv, T};
+    if (threadIdx.x == 0) {
+        mbar_init(s.bar);
+        sh_k = atomicAdd(o.queue, 1);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    if (warp == 0 && sh_k < in.K)
+        stage_begin(s, in, sh_k, lane);
+    while (sh_k < in.K) {
+        const int64_t k = sh_k;
+        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k);
+        C K0 = 0;
+        if (warp == 0) {
+            load_rows(s, MaskSmem{}, sm_in, sr_in, k, T, lane);
+            stage_end(s, in, k, lane, phase);
+            K0 = build_prefix(s, T, pc, lane);
+            int64_t nx = 0;
+            if (lane == 0)
+                nx = atomicAdd(o.queue, 1);
+            nx = __shfl_sync(FULL, nx, 0);
+            if (nx < in.K)
+                stage_begin(s, in, nx, lane);
+            C S;
+            const bool f = base_pass<V, C, MaskSmem, false>(s, mk, T, pc, lane, S);
+            if (lane == 0) {
+                sh_next = nx;
+                sh_S = S;
+                sh_feas = f;
+            }
+        }
+        __syncthreads();
+        const bool feas = sh_feas;
+        const C S0 = sh_S;
+        C S = S0;
+        int64_t evals = 0;
+        int sweeps = 0, moves = 0, ntot = 0;
+        if (feas) {
+            bool dirty = false;
+            for (;;) {
+                bool improved = false;
+                for (int nbh = 1; nbh <= k_max; ++nbh) {
+                    if (warp == 0) {
+                        if (dirty)
+                            base_pass<V, C, MaskSmem, false>(s, mk, T, pc, lane, S);
+                        const int n = enumerate_moves(s, mk, nbh, T, lane);
+                        if (lane == 0) {
+                            sh_n = n;
+                            sh_S = S;
+                        }
+                    }
+                    __syncthreads();
+                    const int n = sh_n;
+                    S = sh_S;
+                    C best = S;
+                    int key = 0x7fffffff;
+                    walk_moves<V, C, MaskSmem, false>(s, mk, T, pc, S, nbh, n, lane, warp,
+                                                      kWarpsPerCta, best, key);
+                    warp_argmin(best, key);
+                    if (lane == 0) {
+                        part_best[warp] = best;
+                        part_key[warp] = key;
+                    }
+                    __syncthreads();
+                    if (warp == 0) {
+                        C b = lane < kWarpsPerCta ? part_best[lane] : S;
+                        int kk = lane < kWarpsPerCta ? part_key[lane] : 0x7fffffff;
+                        warp_argmin(b, kk);
+                        if (kk != 0x7fffffff) {
+                            MaskSmem mw = mk;
+                            apply_slot(mw, nbh, kk, T, lane);
+                            if (lane == 0) {
+                                if (sweeps < o.cap_sweeps)
+                                    atomicAdd(&o.trace_dec[(int64_t)sweeps * k_max + nbh - 1],
+                                              (unsigned long long)(int64_t)(S - b));
+                                else
+                                    atomicExch(o.overflow, 1);
+                            }
+                        }
+                        if (lane == 0) {
+                            sh_key = kk;
+                            sh_best = b;
+                        }
+                    }
+                    __syncthreads();
+                    evals += n;
+                    if (sh_key != 0x7fffffff) {
+                        S = sh_best;
+                        dirty = true;
+                        improved = true;
+                        ++moves;
+                    }
+                }
+                ++sweeps;
+                if (!improved)
+                    break;
+            }
+            if (warp == 0)
+                for (int nbh = 1; nbh <= k_max; ++nbh)
+                    ntot += move_count(mk, nbh, T, lane);
+        } else {
+            sweeps = 1;
+        }
+        if (warp == 0) {
+            store_rows(mk, sm_out, sr_out, k, T, lane);
+            if (lane == 0) {
+                o.start_cost[k] = feas ? (int64_t)(K0 + S0) : RL_INFEASIBLE;
+                o.final_cost[k] = feas ? (int64_t)(K0 + S) : RL_INFEASIBLE;
+                o.evals[k] = evals;
+                o.ntot[k] = ntot;
+                o.sweeps[k] = sweeps;
+                o.moves[k] = moves;
+                sh_k = sh_next;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 #include "vnd_packed.cuh"
 
 // Totals (one block).  summary: 0 final, 1 start, 2 sweeps, 3 evals done,
@@ -601,6 +742,7 @@ struct rl_instance {
     bool timing = false;
     struct GvnsState *gv = nullptr;        // device GVNS state (gvns_impl.cuh)
     double cost_bound = 0.0;               // upper bound of any plan's cost (upload)
+    bool cta_long = true;                  // T > 63, few products: CTA per product (k_vnd_cta)
     bool pack2 = false;                    // T <= 63: two products per warp (vnd_packed.cuh;
                                            // measured slower, kept for A/B)
 };
@@ -772,7 +914,6 @@ extern "C" void rl_instance_destroy(rl_instance *h)
     delete h;
 }
 
-constexpr int kWarpsPerCta = 4;
 
 template <typename V, typename C>
 static int launch_cfg(rl_instance *h, const void *fn, int64_t nprod, int &grid, size_t &smem)
@@ -787,6 +928,21 @@ static int launch_cfg(rl_instance *h, const void *fn, int64_t nprod, int &grid, 
     const int64_t want = (nprod + kWarpsPerCta - 1) / kWarpsPerCta;
     const int64_t cap = (int64_t)h->sms * occ;
     grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+    return 0;
+}
+
+template <typename V, typename C>
+static int launch_cfg_cta(rl_instance *h, const void *fn, int64_t nprod, int &grid, size_t &smem)
+{
+    smem = slot_bytes<V, C>(h->T);
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem));
+    if (occ < 1)
+        return fail(RL_EINVAL, "T=%d needs %zu B shared memory per CTA", h->T, smem);
+    const int64_t cap = (int64_t)h->sms * occ;
+    grid = (int)(nprod < cap ? (nprod > 0 ? nprod : 1) : cap);
     return 0;
 }
 
@@ -808,9 +964,10 @@ static int launch_cfg_pack2(rl_instance *h, const void *fn, int64_t nprod, int &
 
 extern "C" int rl_instance_set_variant(rl_instance *h, int packed)
 {
-    if (!h || packed < 0 || packed > 1)
+    if (!h || packed < 0 || packed > 3)
         return fail(RL_EINVAL, "rl_instance_set_variant: bad arguments");
-    h->pack2 = packed != 0;
+    h->pack2 = (packed & 1) != 0;
+    h->cta_long = (packed & 2) == 0;
     return 0;
 }
 
@@ -1012,6 +1169,11 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     int grid;
     size_t smem;
     const bool pack = std::is_same<Mask, MaskReg>::value && h->pack2;
+    // CTA per product only when the launch is latency-bound (few products):
+    // at C4 scale one warp per product keeps 2.4x more products in flight
+    // and measured 296 ms vs 434 ms
+    const bool cta = std::is_same<Mask, MaskSmem>::value && h->cta_long &&
+                     h->K <= (int64_t)h->sms * 2;
     // skip pays when the launch is latency-bound: fewer products than ~2
     // waves of resident warps (C2, GVNS) -- measured, DESIGN.md section 5
 #ifdef RL_SKIP_ALWAYS
@@ -1022,8 +1184,11 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     const void *fn = pack ? (const void *)k_vnd_pack2<V, C>
                      : skip ? (const void *)k_vnd<V, C, Mask, true>
                             : (const void *)k_vnd<V, C, Mask, false>;
+    if (cta)
+        fn = (const void *)k_vnd_cta<V, C>;
     int rc = pack ? launch_cfg_pack2<V, C>(h, fn, h->K, grid, smem)
-                  : launch_cfg<V, C>(h, fn, h->K, grid, smem);
+             : cta ? launch_cfg_cta<V, C>(h, fn, h->K, grid, smem)
+                   : launch_cfg<V, C>(h, fn, h->K, grid, smem);
     if (rc)
         return rc;
     const int64_t K = h->K;
@@ -1044,6 +1209,9 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     if (pack)
         k_vnd_pack2<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
                                                                   sr_out, k_max, o);
+    else if (cta)
+        k_vnd_cta<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
+                                                                sr_out, k_max, o);
     else if (skip)
         k_vnd<V, C, Mask, true><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in,
                                                                         sm_out, sr_out, k_max, o);

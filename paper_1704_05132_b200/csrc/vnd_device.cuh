@@ -627,38 +627,61 @@ __device__ inline typename PatchOf<Mask>::type patch_of(const Mask &mk, const Mo
 // takes the next unscored move, and every loop iteration advances every
 // busy lane by one segment.  Each lane still scores its moves in
 // increasing slot order, so a strict '<' keeps the earliest on ties.
-template <typename V, typename C, typename Mask, bool Skip = false>
-__device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int T,
-                                       const ProductCosts<C> &pc, C S, int nbh, int lane,
-                                       C &best_out)
+// Move list of neighborhood nbh for the warp's product: N1/N2 are dense
+// (slot = index, returns T), N3/N4 are compacted into s.mv.
+template <typename V, typename C, typename Mask>
+__device__ inline int enumerate_moves(const Slot<V, C> &s, const Mask &mk, int nbh, int T,
+                                      int lane)
 {
-    int n;
-    const bool dense = nbh <= 2;
-    if (dense) {
-        n = T;
-    } else {
-        const int nslots = nbh == 3 ? 4 * T : T;
-        n = 0;
-        for (int base = 0; base < nslots; base += 32) {
-            const int slot = base + lane;
-            const bool ok = slot < nslots && slot_valid(mk, nbh, slot, T);
-            const uint32_t bal = __ballot_sync(FULL, ok);
-            if (ok)
-                s.mv[n + __popc(bal & ((1u << lane) - 1))] = (uint16_t)slot;
-            n += __popc(bal);
-        }
-        __syncwarp();
+    if (nbh <= 2)
+        return T;
+    const int nslots = nbh == 3 ? 4 * T : T;
+    int n = 0;
+    for (int base = 0; base < nslots; base += 32) {
+        const int slot = base + lane;
+        const bool ok = slot < nslots && slot_valid(mk, nbh, slot, T);
+        const uint32_t bal = __ballot_sync(FULL, ok);
+        if (ok)
+            s.mv[n + __popc(bal & ((1u << lane) - 1))] = (uint16_t)slot;
+        n += __popc(bal);
     }
-    C best = S;
-    int key = 0x7fffffff;
+    __syncwarp();
+    return n;
+}
+
+// lexicographic (cost, slot) minimum over the warp
+template <typename C>
+__device__ inline void warp_argmin(C &best, int &key)
+{
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const C ob = __shfl_xor_sync(FULL, best, off);
+        const int ok = __shfl_xor_sync(FULL, key, off);
+        if (ob < best || (ob == best && ok < key)) {
+            best = ob;
+            key = ok;
+        }
+    }
+}
+
+// Score the moves i = wi, wi + nw, wi + 2 nw, ... (< n) of the current list
+// on this warp (nw warps share a product in the CTA variant); per-lane
+// results in best/key (initialise best = S, key = INT_MAX).
+template <typename V, typename C, typename Mask, bool Skip = false>
+__device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
+                                  const ProductCosts<C> &pc, C S, int nbh, int n, int lane,
+                                  int wi, int nw, C &best, int &key)
+{
+    const bool dense = nbh <= 2;
     const unsigned lt = (1u << lane) - 1;
     Walk<V, C, Mask> w;
     int idx = lane, next = 32;
-    bool pend = idx < n, act = false;
+    int gi = idx * nw + wi;
+    bool pend = gi < n, act = false;
     while (__any_sync(FULL, pend | act)) {
         if (pend) {
             pend = false;
-            w.slot = dense ? idx : s.mv[idx];
+            w.slot = dense ? gi : s.mv[gi];
             const MoveDesc d = slot_move(mk, nbh, w.slot, T);
             int a;
             w.nw = patch_of<V, C, Mask>(mk, d, a, w.b);
@@ -731,19 +754,23 @@ __device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int 
         const unsigned m = __ballot_sync(FULL, idle);
         if (idle) {
             idx = next + __popc(m & lt);
-            pend = idx < n;
+            gi = idx * nw + wi;
+            pend = gi < n;
         }
         next += __popc(m);
     }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-        const C ob = __shfl_xor_sync(FULL, best, off);
-        const int ok = __shfl_xor_sync(FULL, key, off);
-        if (ob < best || (ob == best && ok < key)) {
-            best = ob;
-            key = ok;
-        }
-    }
+}
+
+template <typename V, typename C, typename Mask, bool Skip = false>
+__device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int T,
+                                       const ProductCosts<C> &pc, C S, int nbh, int lane,
+                                       C &best_out)
+{
+    const int n = enumerate_moves(s, mk, nbh, T, lane);
+    C best = S;
+    int key = 0x7fffffff;
+    walk_moves<V, C, Mask, Skip>(s, mk, T, pc, S, nbh, n, lane, 0, 1, best, key);
+    warp_argmin(best, key);
     PassResult res;
     res.improved = key != 0x7fffffff;
     res.slot = key;

@@ -176,7 +176,8 @@ def test_c3_k100000_vnd_golden(packed):
     assert _plan_sha(sm, sr) == g["plan_sha"]
 
 
-def test_c4_t520_sample_golden():
+@pytest.mark.parametrize("variant", [0, 2])
+def test_c4_t520_sample_golden(variant):
     """BASELINE config 4 (T=520): products of the K=10,000 seed-0 instance;
     per-product VND is exact by decomposition, so a sample pins the path."""
     g = _big()["k10000_t520_sample"]
@@ -186,7 +187,9 @@ def test_c4_t520_sample_golden():
                     full.setup_cost_m[sub], full.setup_cost_r[sub], full.holding_cost_m[sub],
                     full.holding_cost_r[sub], full.unit_cost_m[sub], full.unit_cost_r[sub])
     start = initial_solution(inst)
-    sm, sr, trace, st = DeviceInstance(inst).vnd(start.setup_m, start.setup_r)
+    dev = DeviceInstance(inst)
+    dev.set_variant(variant)   # 0: CTA per product (default), 2: warp per product
+    sm, sr, trace, st = dev.vnd(start.setup_m, start.setup_r)
     assert st["cost"] == g["cost"]
     assert trace.tolist() == g["trace"]
     assert _plan_sha(sm, sr) == g["plan_sha"]
@@ -210,7 +213,7 @@ def _random_instance(rng, K, T, big=False):
     return Instance(K, T, dem, ret, *c)
 
 
-@pytest.mark.parametrize("packed", [1, 0])
+@pytest.mark.parametrize("packed", [1, 0, 2])
 @pytest.mark.parametrize("seed", range(12))
 def test_fuzz_against_oracle(seed, packed):
     rng = np.random.default_rng(1000 + seed)
@@ -275,10 +278,12 @@ def test_out_of_range_instance_rejected():
         DeviceInstance(inst)
 
 
-def test_mixed_width_t520_paths():
+@pytest.mark.parametrize("variant", [0, 2])
+def test_mixed_width_t520_paths(variant):
     """T=520-style instances take the int32-value / int64-cost path."""
     inst = generate_instance(GeneratorConfig(products=6, periods=300, seed=3))
     dev = DeviceInstance(inst)
+    dev.set_variant(variant)
     assert dev.info["value_bytes"] == 4 and dev.info["cost_bytes"] == 8
     start = initial_solution(inst)
     sm, sr, trace, st = dev.vnd(start.setup_m, start.setup_r)
