@@ -1,4 +1,5 @@
-"""Exhaustive reference optimum on the GPU (mirror of reference oracle.py).
+"""Exhaustive optimum on the GPU (mirror of the reference module oracle.py;
+named exhaustive.py here so it is not confused with the CPU test oracle/).
 
 Products are independent, so the optimum factorizes per product; every one
 of the 2^(2T) setup patterns is decoded with the search's own policy
