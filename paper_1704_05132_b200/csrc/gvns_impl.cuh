@@ -109,6 +109,7 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
             else
                 choice_floyd(rng, g.pop, k_eff, P, g.table + (int64_t)w * g.tsize);
             for (int64_t i = 0; i < k_eff; ++i) {   // distinct touched products
+                RL_ASSERT(P[i] >= 0 && P[i] < g.pop);
                 const int64_t k = (P[i] % g.KT) / T;
                 int j = 0;
                 while (j < n && tp[j] != k)

@@ -35,6 +35,12 @@
 #pragma once
 #include <cstdint>
 #include <type_traits>
+#ifdef RL_DEBUG_CHECKS
+#include <cassert>
+#define RL_ASSERT(x) assert(x)
+#else
+#define RL_ASSERT(x) ((void)0)
+#endif
 
 namespace rl {
 
@@ -175,9 +181,17 @@ struct MaskSmem {
     __device__ bool r(int t) const { return wbit(br, t); }
     __device__ bool setup(int t) const { return wbit(bm, t) | wbit(br, t); }
     // smallest setup period >= x (T if none); needs fresh tables
-    __device__ int next(int x) const { return x >= T ? T : nx[x]; }
+    __device__ int next(int x) const
+    {
+        RL_ASSERT(x >= 0);
+        return x >= T ? T : nx[x];
+    }
     // largest setup period < x (-1 if none); needs fresh tables
-    __device__ int prev(int x) const { return x <= 0 ? -1 : pv[x]; }
+    __device__ int prev(int x) const
+    {
+        RL_ASSERT(x <= T);
+        return x <= 0 ? -1 : pv[x];
+    }
     __device__ void set(int t, bool mv, bool rv, int lane)
     {
         if (lane == 0) {
@@ -367,6 +381,7 @@ template <typename V, typename C>
 __device__ inline bool seg_cost(const V *cd, const V *cr, int T, int u, int v, bool m, bool r,
                                 V X, const ProductCosts<C> &pc, C &c, V &xr)
 {
+    RL_ASSERT(0 <= u && u < v && v <= T);
     const V seg = cd[v] - cd[u];
     const V avail = cr[u + 1] - X;
     xr = r ? vmin(seg, avail) : V(0);
@@ -681,6 +696,7 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
     while (__any_sync(FULL, pend | act)) {
         if (pend) {
             pend = false;
+            RL_ASSERT(gi < n && gi < 4 * T);
             w.slot = dense ? gi : s.mv[gi];
             const MoveDesc d = slot_move(mk, nbh, w.slot, T);
             int a;
