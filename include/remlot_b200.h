@@ -113,6 +113,18 @@ int rl_vnd_device(rl_instance *h, int k_max, const uint8_t *d_sm_in, const uint8
 int rl_vnd_collect(rl_instance *h, int64_t *trace, int64_t trace_cap, int64_t *n_trace,
                    int64_t *stats);
 
+/* rl_instance_update + rl_vnd in one call (same arguments and results): the
+ * host->device copies of the instance and plan rows are cut into product
+ * chunks and overlapped with the descent of the chunks before them on two
+ * compute streams (the e2e path of bench.py; pinned host buffers give the
+ * overlap).  Falls back to the two calls when the new data need wider exact
+ * integers than the handle holds. */
+int rl_vnd_host(rl_instance *h, int k_max, const int64_t *demand, const int64_t *returns,
+                const int64_t *setup_m, const int64_t *setup_r, const int64_t *hold_m,
+                const int64_t *hold_r, const int64_t *unit_m, const int64_t *unit_r,
+                const uint8_t *sm_in, const uint8_t *sr_in, uint8_t *sm_out, uint8_t *sr_out,
+                int64_t *trace, int64_t trace_cap, int64_t *n_trace, int64_t *stats);
+
 /* plan.initial_solution(inst) (plan.py:140-167): lot-for-lot start. */
 int rl_initial_solution(rl_instance *h, uint8_t *sm, uint8_t *sr);
 int rl_initial_solution_device(rl_instance *h, uint8_t *d_sm, uint8_t *d_sr, void *stream);

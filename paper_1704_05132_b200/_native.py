@@ -22,7 +22,7 @@ RL_ERANGE = -4
 EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_instance_set_variant",
            "rl_instance_info", "rl_product_costs", "rl_scan_products", "rl_apply_scan",
-           "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect",
+           "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect", "rl_vnd_host",
            "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_oracle_optimal", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
            "rl_gvns_round", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
            "rl_rng_probe", "rl_launch_count",
@@ -61,6 +61,7 @@ def load():
         "rl_vnd": (I, [P, I, P, P, P, P, P, I64, P, P]),
         "rl_vnd_device": (I, [P, I, P, P, P, P, P]),
         "rl_vnd_collect": (I, [P, P, I64, P, P]),
+        "rl_vnd_host": (I, [P, I] + [P] * 12 + [P, I64, P, P]),
         "rl_initial_solution": (I, [P, P, P]),
         "rl_initial_solution_device": (I, [P, P, P, P]),
         "rl_decode": (I, [P] + [P] * 7),
@@ -191,6 +192,28 @@ class DeviceInstance:
             check(load().rl_vnd(self.h, k_max, ptr(sm), ptr(sr), ptr(out_m.view(np.uint8)),
                                 ptr(out_r.view(np.uint8)), ptr(trace), cap, ptr(nt), ptr(st)),
                   "rl_vnd")
+            if nt[0] <= cap:
+                break
+            cap = int(nt[0])
+        stats = dict(cost=int(st[0]), start_cost=int(st[1]), sweeps=int(st[2]),
+                     evals=int(st[3]), evals_reference=int(st[4]), moves=int(st[5]),
+                     products=int(st[6]), kernel_ns=int(st[7]), ntot_sum=int(st[8]))
+        return out_m, out_r, trace[:nt[0]].copy(), stats
+
+    def vnd_host(self, inst, sm, sr, k_max=4, trace_cap=None):
+        """update(inst) + vnd(sm, sr) in one pipelined call (rl_vnd_host)."""
+        arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in inst.arrays()]
+        sm, sr = u8(sm), u8(sr)
+        out_m = np.empty((self.K, self.T), np.bool_)
+        out_r = np.empty((self.K, self.T), np.bool_)
+        cap = trace_cap or 4096
+        while True:
+            trace = np.empty(cap, np.int64)
+            nt = np.zeros(1, np.int64)
+            st = np.zeros(9, np.int64)
+            check(load().rl_vnd_host(self.h, k_max, *[ptr(a) for a in arrays], ptr(sm), ptr(sr),
+                                     ptr(out_m.view(np.uint8)), ptr(out_r.view(np.uint8)),
+                                     ptr(trace), cap, ptr(nt), ptr(st)), "rl_vnd_host")
             if nt[0] <= cap:
                 break
             cap = int(nt[0])

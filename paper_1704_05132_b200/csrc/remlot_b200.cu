@@ -308,7 +308,8 @@ struct VndOut {
     unsigned long long *trace_dec;   // [cap_sweeps * k_max]
     int64_t cap_sweeps;
     int *overflow;
-    int *queue;
+    int *queue;              // products k_lo + atomicAdd(queue) < k_hi
+    int64_t k_lo, k_hi;
 };
 
 // Persistent resident VND.  Every warp pulls products from a global queue
@@ -346,11 +347,11 @@ __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstVie
 
     int64_t k = 0;
     if (lane == 0)
-        k = atomicAdd(o.queue, 1);
+        k = o.k_lo + atomicAdd(o.queue, 1);
     k = __shfl_sync(FULL, k, 0);
-    if (k < in.K)
+    if (k < o.k_hi)
         stage_begin(s, in, k, lane);
-    while (k < in.K) {
+    while (k < o.k_hi) {
         const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k);
         Mask mk = load_rows(s, Mask{}, sm_in, sr_in, k, T, lane);
         stage_end(s, in, k, lane, phase);
@@ -358,9 +359,9 @@ __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstVie
         // prefetch the next product's rows into the (now consumed) stage
         int64_t next = 0;
         if (lane == 0)
-            next = atomicAdd(o.queue, 1);
+            next = o.k_lo + atomicAdd(o.queue, 1);
         next = __shfl_sync(FULL, next, 0);
-        if (next < in.K)
+        if (next < o.k_hi)
             stage_begin(s, in, next, lane);
 
         C S, S0;
@@ -404,13 +405,13 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
     const MaskSmem mk{s.bm, s.br, s.nx, s.pv, T};
     if (threadIdx.x == 0) {
         mbar_init(s.bar);
-        sh_k = atomicAdd(o.queue, 1);
+        sh_k = o.k_lo + atomicAdd(o.queue, 1);
     }
     __syncthreads();
     uint32_t phase = 0;
-    if (warp == 0 && sh_k < in.K)
+    if (warp == 0 && sh_k < o.k_hi)
         stage_begin(s, in, sh_k, lane);
-    while (sh_k < in.K) {
+    while (sh_k < o.k_hi) {
         const int64_t k = sh_k;
         const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k);
         C K0 = 0;
@@ -420,9 +421,9 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
             K0 = build_prefix(s, T, pc, lane);
             int64_t nx = 0;
             if (lane == 0)
-                nx = atomicAdd(o.queue, 1);
+                nx = o.k_lo + atomicAdd(o.queue, 1);
             nx = __shfl_sync(FULL, nx, 0);
-            if (nx < in.K)
+            if (nx < o.k_hi)
                 stage_begin(s, in, nx, lane);
             C S;
             const bool f = base_pass<V, C, MaskSmem, false>(s, mk, T, pc, lane, S);
@@ -720,10 +721,13 @@ __global__ void k_list_moves(int nbh, int T, const uint8_t *sm, const uint8_t *s
 
 // ------------------------------------------------------------------ handle
 
+constexpr int kMaxChunks = 4;   // rl_vnd_host pipeline depth
+
 struct rl_instance {
     int64_t K = 0;
     int T = 0, vbytes = 8, cbytes = 8, device = 0, sms = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, stream2 = nullptr, stream3 = nullptr;
+    cudaEvent_t evc[kMaxChunks + 2] = {};   // rl_vnd_host: chunk copies landed, joins
     int64_t *dem64 = nullptr, *ret64 = nullptr, *cost6 = nullptr;
     void *dem = nullptr, *ret = nullptr;   // V typed (alias dem64/ret64 when V = int64)
     uint8_t *plan = nullptr;               // 4 x K x T: sm_in, sr_in, sm_out, sr_out
@@ -844,6 +848,10 @@ extern "C" int rl_instance_create(int64_t K, int64_t T, const int64_t *demand,
         e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
         const size_t kt = (size_t)K * T;
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking);
+        for (auto &ev : h->evc)
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaMalloc(&h->dem64, kt * 8 * 2);
         if (e == cudaSuccess) {
             h->ret64 = h->dem64 + kt;
@@ -910,6 +918,13 @@ extern "C" void rl_instance_destroy(rl_instance *h)
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->stream)
         cudaStreamDestroy(h->stream);
+    if (h->stream2)
+        cudaStreamDestroy(h->stream2);
+    if (h->stream3)
+        cudaStreamDestroy(h->stream3);
+    for (auto ev : h->evc)
+        if (ev)
+            cudaEventDestroy(ev);
     gvns_free(h->gv);
     delete h;
 }
@@ -1162,35 +1177,8 @@ extern "C" int rl_apply_scan(rl_instance *h, int64_t lo, int64_t hi, const int64
     return 0;
 }
 
-template <typename V, typename C, typename Mask>
-static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t *sr_in,
-                  uint8_t *sm_out, uint8_t *sr_out, cudaStream_t st)
+static VndOut vnd_out(rl_instance *h, int64_t lo, int64_t hi, int *queue)
 {
-    int grid;
-    size_t smem;
-    const bool pack = std::is_same<Mask, MaskReg>::value && h->pack2;
-    // CTA per product only when the launch is latency-bound (few products):
-    // at C4 scale one warp per product keeps 2.4x more products in flight
-    // and measured 296 ms vs 434 ms (DESIGN.md section 5)
-    const bool cta = std::is_same<Mask, MaskSmem>::value && h->cta_long &&
-                     h->K <= (int64_t)h->sms * 2;
-    // skip pays when the launch is latency-bound: fewer products than ~2
-    // waves of resident warps (C2, GVNS) -- measured, DESIGN.md section 5
-#ifdef RL_SKIP_ALWAYS
-    const bool skip = std::is_same<Mask, MaskReg>::value;
-#else
-    const bool skip = std::is_same<Mask, MaskReg>::value && h->K < (int64_t)h->sms * 64;
-#endif
-    const void *fn = pack ? (const void *)k_vnd_pack2<V, C>
-                     : skip ? (const void *)k_vnd<V, C, Mask, true>
-                            : (const void *)k_vnd<V, C, Mask, false>;
-    if (cta)
-        fn = (const void *)k_vnd_cta<V, C>;
-    int rc = pack ? launch_cfg_pack2<V, C>(h, fn, h->K, grid, smem)
-             : cta ? launch_cfg_cta<V, C>(h, fn, h->K, grid, smem)
-                   : launch_cfg<V, C>(h, fn, h->K, grid, smem);
-    if (rc)
-        return rc;
     const int64_t K = h->K;
     VndOut o;
     o.start_cost = h->p64;
@@ -1202,10 +1190,44 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     o.trace_dec = h->trace_dec;
     o.cap_sweeps = h->cap_sweeps;
     o.overflow = h->ints + 1;
-    o.queue = h->ints;
-    CK(cudaMemsetAsync(h->ints, 0, 2 * sizeof(int), st));
-    CK(cudaMemsetAsync(h->trace_dec, 0, (size_t)h->cap_sweeps * k_max * 8, st));
-    CK(cudaEventRecord(h->ev0, st));
+    o.queue = queue;
+    o.k_lo = lo;
+    o.k_hi = hi;
+    return o;
+}
+
+// Launch the VND kernel variant for products [lo, hi) (queue reset by caller).
+template <typename V, typename C, typename Mask>
+static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t *sr_in,
+                            uint8_t *sm_out, uint8_t *sr_out, int64_t lo, int64_t hi, int *queue,
+                            cudaStream_t st)
+{
+    int grid;
+    size_t smem;
+    const int64_t nprod = hi - lo;
+    const bool pack = std::is_same<Mask, MaskReg>::value && h->pack2;
+    // CTA per product only when the launch is latency-bound (few products):
+    // at C4 scale one warp per product keeps 2.4x more products in flight
+    // and measured 296 ms vs 434 ms (DESIGN.md section 5)
+    const bool cta = std::is_same<Mask, MaskSmem>::value && h->cta_long &&
+                     nprod <= (int64_t)h->sms * 2;
+    // skip pays when the launch is latency-bound: fewer products than ~2
+    // waves of resident warps (C2, GVNS) -- measured, DESIGN.md section 5
+#ifdef RL_SKIP_ALWAYS
+    const bool skip = std::is_same<Mask, MaskReg>::value;
+#else
+    const bool skip = std::is_same<Mask, MaskReg>::value && nprod < (int64_t)h->sms * 64;
+#endif
+    const void *fn = pack ? (const void *)k_vnd_pack2<V, C>
+                     : cta ? (const void *)k_vnd_cta<V, C>
+                     : skip ? (const void *)k_vnd<V, C, Mask, true>
+                            : (const void *)k_vnd<V, C, Mask, false>;
+    int rc = pack ? launch_cfg_pack2<V, C>(h, fn, nprod, grid, smem)
+             : cta ? launch_cfg_cta<V, C>(h, fn, nprod, grid, smem)
+                   : launch_cfg<V, C>(h, fn, nprod, grid, smem);
+    if (rc)
+        return rc;
+    const VndOut o = vnd_out(h, lo, hi, queue);
     if (pack)
         k_vnd_pack2<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
                                                                   sr_out, k_max, o);
@@ -1219,8 +1241,22 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
         k_vnd<V, C, Mask, false><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in,
                                                                          sm_out, sr_out, k_max, o);
     CKL();
+    return 0;
+}
+
+template <typename V, typename C, typename Mask>
+static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t *sr_in,
+                  uint8_t *sm_out, uint8_t *sr_out, cudaStream_t st)
+{
+    CK(cudaMemsetAsync(h->ints, 0, 2 * sizeof(int), st));
+    CK(cudaMemsetAsync(h->trace_dec, 0, (size_t)h->cap_sweeps * k_max * 8, st));
+    CK(cudaEventRecord(h->ev0, st));
+    int rc = launch_vnd_range<V, C, Mask>(h, k_max, sm_in, sr_in, sm_out, sr_out, 0, h->K,
+                                          h->ints, st);
+    if (rc)
+        return rc;
     CK(cudaEventRecord(h->ev1, st));
-    k_vnd_finalize<<<1, 1024, 0, st>>>(K, o, h->summary);
+    k_vnd_finalize<<<1, 1024, 0, st>>>(h->K, vnd_out(h, 0, h->K, h->ints), h->summary);
     CKL();
     return 0;
 }
@@ -1316,6 +1352,157 @@ extern "C" int rl_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uin
     CK(cudaMemcpyAsync(sr_out, h->plan + 3 * kt, kt, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return 0;
+}
+
+// Chunk of a streamed upload: per product check that the handle's exact
+// widths still hold (else flag -> the caller falls back to a full upload)
+// and narrow demand/returns to int32 when that is the stored width.
+__global__ void k_check_narrow(int64_t lo, int64_t hi, int T, int64_t K, const int64_t *dem,
+                               const int64_t *ret, const int64_t *c6, int vbytes, int cbytes,
+                               int32_t *dem32, int32_t *ret32, int *bad,
+                               unsigned long long *bounds)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t k = lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < hi;
+         k += nw) {
+        double sd = 0.0, sr = 0.0;
+        bool neg = false;
+        for (int t = lane; t < T; t += 32) {
+            const int64_t d = dem[k * T + t], r = ret[k * T + t];
+            neg |= d < 0 || r < 0;
+            sd += (double)d;
+            sr += (double)r;
+            if (vbytes == 4) {
+                dem32[k * T + t] = (int32_t)d;
+                ret32[k * T + t] = (int32_t)r;
+            }
+        }
+        for (int off = 16; off; off >>= 1) {
+            sd += __shfl_xor_sync(FULL, sd, off);
+            sr += __shfl_xor_sync(FULL, sr, off);
+        }
+        neg = __any_sync(FULL, neg);
+        if (lane == 0) {
+            double c[6];
+            for (int i = 0; i < 6; ++i) {
+                c[i] = (double)c6[i * K + k];
+                neg |= c6[i * K + k] < 0;
+            }
+            const double B = (double)T * (c[0] + c[1]) + (c[4] + c[5]) * sd +
+                             (double)T * c[2] * sd + (double)T * c[3] * sr;
+            const double vlim = std::ldexp(1.0, vbytes == 4 ? 28 : 60);
+            const double clim = std::ldexp(1.0, cbytes == 4 ? 30 : 61);
+            if (neg || !(sd + sr < vlim) || !(B < clim))
+                atomicExch(bad, 1);
+            atomicMax(&bounds[0], (unsigned long long)__double_as_longlong(sd + sr));
+            atomicMax(&bounds[1], (unsigned long long)__double_as_longlong(B));
+        }
+    }
+}
+
+template <typename V, typename C, typename Mask>
+static int do_vnd_chunks(rl_instance *h, int k_max, int nchunks)
+{
+    const int64_t K = h->K;
+    const int T = h->T;
+    const size_t kt = (size_t)K * T;
+    for (int c = 0; c < nchunks; ++c) {
+        cudaStream_t st = (c & 1) ? h->stream2 : h->stream;
+        const int64_t lo = K * c / nchunks, hi = K * (c + 1) / nchunks;
+        CK(cudaStreamWaitEvent(st, h->evc[c], 0));
+        k_check_narrow<<<h->sms, 256, 0, st>>>(lo, hi, T, K, h->dem64, h->ret64, h->cost6,
+                                               h->vbytes, h->cbytes, (int32_t *)h->dem,
+                                               (int32_t *)h->ret, h->ints + 3, h->bounds);
+        CKL();
+        if (c == 0)
+            CK(cudaEventRecord(h->ev0, st));
+        int rc = launch_vnd_range<V, C, Mask>(h, k_max, h->plan, h->plan + kt, h->plan + 2 * kt,
+                                              h->plan + 3 * kt, lo, hi, h->ints + 4 + c, st);
+        if (rc)
+            return rc;
+    }
+    return 0;
+}
+
+// vnd() from host buffers with the uploads pipelined against the descent:
+// products are cut into chunks; a copy stream lands chunk c's instance and
+// plan rows while the two compute streams run the chunks before it, and each
+// chunk's result rows go back as soon as its kernel ends.  Same results as
+// rl_instance_update + rl_vnd, which it falls back to when the new data do
+// not fit the handle's exact integer widths (or the trace buffer overflows).
+extern "C" int rl_vnd_host(rl_instance *h, int k_max, const int64_t *demand,
+                           const int64_t *returns, const int64_t *setup_m, const int64_t *setup_r,
+                           const int64_t *hold_m, const int64_t *hold_r, const int64_t *unit_m,
+                           const int64_t *unit_r, const uint8_t *sm_in, const uint8_t *sr_in,
+                           uint8_t *sm_out, uint8_t *sr_out, int64_t *trace, int64_t trace_cap,
+                           int64_t *n_trace, int64_t *stats)
+{
+    (void)cudaGetLastError();
+    if (!h || !demand || !returns || !setup_m || !setup_r || !hold_m || !hold_r || !unit_m ||
+        !unit_r || !sm_in || !sr_in || !sm_out || !sr_out || !stats)
+        return fail(RL_EINVAL, "rl_vnd_host: bad arguments");
+    if (k_max < 1 || k_max > 4)
+        return fail(RL_EINVAL, "k_max must be in 1..4, got %d", k_max);
+    CK(cudaSetDevice(h->device));
+    const int64_t K = h->K;
+    const int T = h->T;
+    const size_t kt = (size_t)K * T;
+    const int nchunks = K >= (int64_t)kMaxChunks * 64 * h->sms ? kMaxChunks : 1;
+    cudaStream_t s0 = h->stream, s1 = h->stream2, sc = h->stream3;
+    cudaEvent_t join = h->evc[kMaxChunks], start = h->evc[kMaxChunks + 1];
+    // order after any earlier work on the handle's stream
+    CK(cudaEventRecord(start, s0));
+    CK(cudaStreamWaitEvent(sc, start, 0));
+    CK(cudaStreamWaitEvent(s1, start, 0));
+    const int64_t *cost[6] = {setup_m, setup_r, hold_m, hold_r, unit_m, unit_r};
+    for (int i = 0; i < 6; ++i)
+        CK(cudaMemcpyAsync(h->cost6 + i * K, cost[i], K * 8, cudaMemcpyHostToDevice, sc));
+    CK(cudaMemsetAsync(h->ints, 0, 16 * sizeof(int), sc));
+    CK(cudaMemsetAsync(h->bounds, 0, 2 * sizeof(unsigned long long), sc));
+    CK(cudaMemsetAsync(h->trace_dec, 0, (size_t)h->cap_sweeps * k_max * 8, sc));
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t lo = K * c / nchunks, hi = K * (c + 1) / nchunks;
+        const size_t off = (size_t)lo * T, n = (size_t)(hi - lo) * T;
+        CK(cudaMemcpyAsync(h->dem64 + off, demand + off, n * 8, cudaMemcpyHostToDevice, sc));
+        CK(cudaMemcpyAsync(h->ret64 + off, returns + off, n * 8, cudaMemcpyHostToDevice, sc));
+        CK(cudaMemcpyAsync(h->plan + off, sm_in + off, n, cudaMemcpyHostToDevice, sc));
+        CK(cudaMemcpyAsync(h->plan + kt + off, sr_in + off, n, cudaMemcpyHostToDevice, sc));
+        CK(cudaEventRecord(h->evc[c], sc));
+    }
+    h->last_kmax = k_max;
+    int rc = RL_DISPATCH_M(h, do_vnd_chunks, h, k_max, nchunks);
+    if (rc)
+        return rc;
+    for (int c = 0; c < nchunks; ++c) {
+        cudaStream_t st = (c & 1) ? s1 : s0;
+        const int64_t lo = K * c / nchunks, hi = K * (c + 1) / nchunks;
+        const size_t off = (size_t)lo * T, n = (size_t)(hi - lo) * T;
+        CK(cudaMemcpyAsync(sm_out + off, h->plan + 2 * kt + off, n, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(sr_out + off, h->plan + 3 * kt + off, n, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaEventRecord(join, s1));
+    CK(cudaStreamWaitEvent(s0, join, 0));
+    CK(cudaEventRecord(h->ev1, s0));
+    k_vnd_finalize<<<1, 1024, 0, s0>>>(K, vnd_out(h, 0, K, h->ints), h->summary);
+    CKL();
+    int bad = 0;
+    unsigned long long hb[2];
+    CK(cudaMemcpyAsync(&bad, h->ints + 3, sizeof bad, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(hb, h->bounds, sizeof hb, cudaMemcpyDeviceToHost, s0));
+    CK(cudaStreamSynchronize(s0));
+    if (!bad) {
+        memcpy(&h->cost_bound, &hb[1], 8);
+        rc = rl_vnd_collect(h, trace, trace_cap, n_trace, stats);
+    }
+    if (bad || rc == RL_ERANGE) {
+        rc = rl_instance_update(h, demand, returns, setup_m, setup_r, hold_m, hold_r, unit_m,
+                                unit_r);
+        if (rc)
+            return rc;
+        return rl_vnd(h, k_max, sm_in, sr_in, sm_out, sr_out, trace, trace_cap, n_trace, stats);
+    }
+    return rc;
 }
 
 template <typename V, typename C>

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(128, 4) k_vnd_pack2(InstView<V> in, const uint
         mbar_init(so.bar);
     __syncwarp();
     uint32_t phase = 0;
-    const int64_t NONE = in.K;
+    const int64_t NONE = o.k_hi;
 
     // lockstep state of both products, warp-uniform (held by every lane)
     int64_t kk[2] = {NONE, NONE}, evals[2] = {0, 0};
@@ -218,9 +218,9 @@ __global__ void __launch_bounds__(128, 4) k_vnd_pack2(InstView<V> in, const uint
     // each group prefetches its next product's rows (TMA) into its stage
     int64_t nxt = 0;
     if (q == 0)
-        nxt = atomicAdd(o.queue, 1);
+        nxt = o.k_lo + atomicAdd(o.queue, 1);
     nxt = __shfl_sync(FULL, nxt, 16 * g);
-    if (nxt < in.K)
+    if (nxt < o.k_hi)
         stage_begin(so, in, nxt, q);
 
     for (;;) {
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(128, 4) k_vnd_pack2(InstView<V> in, const uint
             C K0o = 0;
             if (w_own) {
                 k_own = nxt;
-                const bool ld = k_own < in.K;
+                const bool ld = k_own < o.k_hi;
                 if (ld) {
                     stage_end16(so, in, k_own, q, phase, gmask);
                     pco = load_costs<C>(in.cost6, in.K, k_own);
@@ -247,9 +247,9 @@ __global__ void __launch_bounds__(128, 4) k_vnd_pack2(InstView<V> in, const uint
                     K0o = build_prefix16(so, T, pco, q, gmask);
                     int64_t n2 = 0;
                     if (q == 0)
-                        n2 = atomicAdd(o.queue, 1);
+                        n2 = o.k_lo + atomicAdd(o.queue, 1);
                     nxt = __shfl_sync(gmask, n2, 16 * g);
-                    if (nxt < in.K)
+                    if (nxt < o.k_hi)
                         stage_begin(so, in, nxt, q);
                 }
             }

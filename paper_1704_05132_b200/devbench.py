@@ -22,12 +22,13 @@ def _pinned(torch, a):
     return t, arr
 
 
-def e2e_steps(torch, _native, dev, shard, steps, world, dist, coll="cuda"):
+def e2e_steps(torch, _native, dev, shard, steps, world, dist, coll="cuda", pipelined=True):
     """Time `steps` end-to-end descents through the C ABI with pinned host
-    buffers: each step uploads the instance (rl_instance_update) and the
-    start plan, runs the VND (rl_vnd) and reads back the final plan, trace
-    and stats.  Returns (max-over-ranks total ms, h2d bytes, d2h bytes) for
-    the whole job."""
+    buffers: each step uploads the instance and the start plan, runs the VND
+    and reads back the final plan, trace and stats -- one rl_vnd_host call
+    (uploads chunked and overlapped with the descent) or, pipelined=False,
+    rl_instance_update + rl_vnd.  Returns (max-over-ranks total ms, h2d
+    bytes, d2h bytes) for the whole job."""
     lib = _native.load()
     keep = []
     arrays = []
@@ -47,6 +48,11 @@ def e2e_steps(torch, _native, dev, shard, steps, world, dist, coll="cuda"):
     P = _native.ptr
 
     def one():
+        if pipelined:
+            _native.check(lib.rl_vnd_host(dev.h, 4, *[P(a) for a in arrays], P(sm), P(sr), P(om),
+                                          P(orr), P(trace), len(trace), P(nt), P(st)),
+                          "rl_vnd_host")
+            return
         _native.check(lib.rl_instance_update(dev.h, *[P(a) for a in arrays]),
                       "rl_instance_update")
         _native.check(lib.rl_vnd(dev.h, 4, P(sm), P(sr), P(om), P(orr), P(trace), len(trace),

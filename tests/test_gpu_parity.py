@@ -291,3 +291,52 @@ def test_mixed_width_t520_paths(variant):
     assert st["cost"] == ocost
     np.testing.assert_array_equal(trace, otrace)
     np.testing.assert_array_equal(sm, om)
+
+
+def test_c3_vnd_host_pipelined_golden():
+    """rl_vnd_host (chunked uploads overlapped with the descent, the bench's
+    e2e call) reproduces the C3 golden, then serves a different instance of
+    the same shape on the same handle exactly like a fresh handle does."""
+    g = _big()["k100000_t52"]
+    inst = generate_instance(GeneratorConfig(products=100000, periods=52, seed=0))
+    other = generate_instance(GeneratorConfig(products=100000, periods=52, seed=5))
+    start = initial_solution(inst)
+    dev = DeviceInstance(other)   # handle holds a different instance
+    sm, sr, trace, st = dev.vnd_host(inst, start.setup_m, start.setup_r)
+    assert st["cost"] == g["cost"]
+    assert trace.tolist() == g["trace"]
+    assert _plan_sha(sm, sr) == g["plan_sha"]
+    s2 = initial_solution(other)
+    got = dev.vnd_host(other, s2.setup_m, s2.setup_r, k_max=3)
+    want = DeviceInstance(other).vnd(s2.setup_m, s2.setup_r, k_max=3)
+    assert got[3]["cost"] == want[3]["cost"]
+    np.testing.assert_array_equal(got[2], want[2])
+    np.testing.assert_array_equal(got[0], want[0])
+    np.testing.assert_array_equal(got[1], want[1])
+    assert got[3]["evals_reference"] == want[3]["evals_reference"]
+
+
+def test_vnd_host_width_fallback():
+    """New data wider than the handle's int32 layout fall back to a full
+    upload (int64 path) with identical results; negative data are refused."""
+    rng = np.random.default_rng(5)
+    small = _random_instance(rng, 17, 40)
+    wide = _random_instance(rng, 17, 40, big=True)
+    dev = DeviceInstance(small)
+    assert dev.info["value_bytes"] == 4
+    start = initial_solution(wide)
+    sm, sr, trace, st = dev.vnd_host(wide, start.setup_m, start.setup_r)
+    om, orr, ocost, otrace, ost = oracle.vnd(wide, start.setup_m, start.setup_r)
+    assert st["cost"] == ocost
+    np.testing.assert_array_equal(trace, otrace)
+    np.testing.assert_array_equal(sm, om)
+    np.testing.assert_array_equal(sr, orr)
+    # and back to small data on the (now int64) handle
+    s0 = initial_solution(small)
+    sm, sr, trace, st = dev.vnd_host(small, s0.setup_m, s0.setup_r)
+    om, orr, ocost, otrace, _ = oracle.vnd(small, s0.setup_m, s0.setup_r)
+    assert st["cost"] == ocost
+    np.testing.assert_array_equal(trace, otrace)
+    bad = Instance(17, 40, -np.ones((17, 40), np.int64), small.returns, *small.arrays()[2:])
+    with pytest.raises(ValueError):
+        dev.vnd_host(bad, s0.setup_m, s0.setup_r)
