@@ -125,6 +125,21 @@ int rl_vnd_host(rl_instance *h, int k_max, const int64_t *demand, const int64_t 
                 const uint8_t *sm_in, const uint8_t *sr_in, uint8_t *sm_out, uint8_t *sr_out,
                 int64_t *trace, int64_t trace_cap, int64_t *n_trace, int64_t *stats);
 
+/* model.generate_instance(GeneratorConfig(...)) (model.py:115-153) on the
+ * device: the same numpy Philox stream and Lemire draws, bit-identical
+ * arrays.  ranges = {setup lo, hi, holding lo, hi, unit lo, hi} (inclusive).
+ * The handle keeps products [lo, hi) of the K-product instance (lo = 0,
+ * hi = K for all of it).  RL_EINVAL for configs GeneratorConfig rejects and
+ * for ranges of 2^32-1 or more (numpy's 64-bit draw path). */
+int rl_generate_instance(int64_t K, int64_t T, uint64_t seed, int64_t demand_max,
+                         double return_ratio, const int64_t *ranges, int64_t lo, int64_t hi,
+                         rl_instance **out);
+
+/* The handle's instance back in host arrays (K x T, K x T, six K-vectors). */
+int rl_instance_download(rl_instance *h, int64_t *demand, int64_t *returns, int64_t *setup_m,
+                         int64_t *setup_r, int64_t *hold_m, int64_t *hold_r, int64_t *unit_m,
+                         int64_t *unit_r);
+
 /* plan.initial_solution(inst) (plan.py:140-167): lot-for-lot start. */
 int rl_initial_solution(rl_instance *h, uint8_t *sm, uint8_t *sr);
 int rl_initial_solution_device(rl_instance *h, uint8_t *d_sm, uint8_t *d_sr, void *stream);

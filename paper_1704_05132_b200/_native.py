@@ -25,7 +25,7 @@ EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect", "rl_vnd_host",
            "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_oracle_optimal", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
            "rl_gvns_round", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
-           "rl_rng_probe", "rl_launch_count",
+           "rl_rng_probe", "rl_launch_count", "rl_generate_instance", "rl_instance_download",
            "rl_last_error")
 
 _lib = None
@@ -75,6 +75,9 @@ def load():
         "rl_gvns_state": (I, [P, I, P, P, P]),
         "rl_rng_probe": (I, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, I64, I64, I64, P]),
         "rl_launch_count": (I64, [P]),
+        "rl_generate_instance": (I, [I64, I64, ctypes.c_uint64, I64, ctypes.c_double, P, I64,
+                                     I64, ctypes.POINTER(P)]),
+        "rl_instance_download": (I, [P] * 9),
         "rl_last_error": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -111,15 +114,46 @@ class DeviceInstance:
 
     def __init__(self, inst):
         lib = load()
-        self.K = int(inst.products)
-        self.T = int(inst.periods)
         arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in inst.arrays()]
         h = ctypes.c_void_p()
-        check(lib.rl_instance_create(self.K, self.T, *[ptr(a) for a in arrays],
-                                     ctypes.byref(h)), "rl_instance_create")
+        check(lib.rl_instance_create(int(inst.products), int(inst.periods),
+                                     *[ptr(a) for a in arrays], ctypes.byref(h)),
+              "rl_instance_create")
+        self._bind(h)
+
+    @classmethod
+    def generate(cls, config, lo=0, hi=None):
+        """model.generate_instance(config) drawn on the device (bit-identical
+        arrays), keeping products [lo, hi) -- a rank's shard of the global
+        instance without generating or uploading it on the host."""
+        hi = config.products if hi is None else hi
+        c = config
+        ranges = np.array(c.setup_cost_range + c.holding_cost_range + c.unit_cost_range,
+                          np.int64)
+        h = ctypes.c_void_p()
+        check(load().rl_generate_instance(c.products, c.periods, c.seed & ((1 << 64) - 1),
+                                          c.demand_max, c.return_ratio, ptr(ranges), lo, hi,
+                                          ctypes.byref(h)), "rl_generate_instance")
+        self = cls.__new__(cls)
+        self._bind(h)
+        return self
+
+    def download(self):
+        """The handle's instance as a host Instance."""
+        from .model import Instance
+        dem = np.empty((self.K, self.T), np.int64)
+        ret = np.empty((self.K, self.T), np.int64)
+        vec = [np.empty(self.K, np.int64) for _ in range(6)]
+        check(load().rl_instance_download(self.h, ptr(dem), ptr(ret), *[ptr(v) for v in vec]),
+              "rl_instance_download")
+        return Instance(self.K, self.T, dem, ret, *vec)
+
+    def _bind(self, h):
         self.h = h
         info = np.zeros(6, np.int64)
-        check(lib.rl_instance_info(h, ptr(info)), "rl_instance_info")
+        check(load().rl_instance_info(h, ptr(info)), "rl_instance_info")
+        self.K = int(info[0])
+        self.T = int(info[1])
         self.info = dict(K=int(info[0]), T=int(info[1]), value_bytes=int(info[2]),
                          cost_bytes=int(info[3]), sms=int(info[4]), warps_per_cta=int(info[5]))
 

@@ -767,15 +767,11 @@ static int ensure_trace(rl_instance *h, int64_t cap_sweeps, int k_max)
     return 0;
 }
 
-static int upload(rl_instance *h, const int64_t *demand, const int64_t *returns,
-                  const int64_t *const cost[6])
+// Range check + exact-width selection + narrowing of the int64 rows already
+// in dem64/ret64/cost6 (the device half of an upload).
+static int prepare(rl_instance *h)
 {
     const size_t kt = (size_t)h->K * h->T;
-    CK(cudaMemcpyAsync(h->dem64, demand, kt * 8, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemcpyAsync(h->ret64, returns, kt * 8, cudaMemcpyHostToDevice, h->stream));
-    for (int i = 0; i < 6; ++i)
-        CK(cudaMemcpyAsync(h->cost6 + i * h->K, cost[i], h->K * 8, cudaMemcpyHostToDevice,
-                           h->stream));
     CK(cudaMemsetAsync(h->bounds, 0, 3 * sizeof(unsigned long long), h->stream));
     CK(cudaMemsetAsync(h->ints, 0, 4 * sizeof(int), h->stream));
     const int blk = 256;
@@ -824,6 +820,64 @@ static int upload(rl_instance *h, const int64_t *demand, const int64_t *returns,
     return 0;
 }
 
+static int upload(rl_instance *h, const int64_t *demand, const int64_t *returns,
+                  const int64_t *const cost[6])
+{
+    const size_t kt = (size_t)h->K * h->T;
+    CK(cudaMemcpyAsync(h->dem64, demand, kt * 8, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->ret64, returns, kt * 8, cudaMemcpyHostToDevice, h->stream));
+    for (int i = 0; i < 6; ++i)
+        CK(cudaMemcpyAsync(h->cost6 + i * h->K, cost[i], h->K * 8, cudaMemcpyHostToDevice,
+                           h->stream));
+    return prepare(h);
+}
+
+// Streams, events and every K x T / K buffer of a handle (h->K, h->T set).
+static int alloc_instance(rl_instance *h)
+{
+    const int64_t K = h->K;
+    const size_t kt = (size_t)K * h->T;
+    cudaError_t e = cudaGetDevice(&h->device);
+    if (e != cudaSuccess)
+        return fail(RL_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking);
+    for (auto &ev : h->evc)
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMalloc(&h->dem64, kt * 8 * 2);
+    if (e == cudaSuccess) {
+        h->ret64 = h->dem64 + kt;
+        e = cudaMalloc(&h->cost6, K * 8 * 6);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&h->plan, kt * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&h->p64, K * 8 * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&h->p32, K * 4 * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&h->ints, 16 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&h->summary, 16 * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&h->bounds, 4 * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&h->scan_i64, K * 8 * 3);
+    if (e == cudaSuccess) e = cudaMalloc(&h->scan_u8, K * 4);
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+    if (e != cudaSuccess)
+        return fail(RL_ECUDA, "rl_instance_create: %s", cudaGetErrorString(e));
+    return ensure_trace(h, 1024, 4);
+}
+
+static int finish_create(rl_instance *h, int rc, rl_instance **out)
+{
+    if (rc) {
+        std::string keep = g_err;
+        rl_instance_destroy(h);
+        g_err = keep;
+        return rc;
+    }
+    *out = h;
+    return 0;
+}
+
 extern "C" int rl_instance_create(int64_t K, int64_t T, const int64_t *demand,
                                   const int64_t *returns, const int64_t *setup_m,
                                   const int64_t *setup_r, const int64_t *hold_m,
@@ -838,52 +892,12 @@ extern "C" int rl_instance_create(int64_t K, int64_t T, const int64_t *demand,
     rl_instance *h = new rl_instance();
     h->K = K;
     h->T = (int)T;
-    int rc = 0;
-    do {
-        cudaError_t e = cudaGetDevice(&h->device);
-        if (e != cudaSuccess) {
-            rc = fail(RL_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
-            break;
-        }
-        e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
-        const size_t kt = (size_t)K * T;
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking);
-        for (auto &ev : h->evc)
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaMalloc(&h->dem64, kt * 8 * 2);
-        if (e == cudaSuccess) {
-            h->ret64 = h->dem64 + kt;
-            e = cudaMalloc(&h->cost6, K * 8 * 6);
-        }
-        if (e == cudaSuccess) e = cudaMalloc(&h->plan, kt * 4);
-        if (e == cudaSuccess) e = cudaMalloc(&h->p64, K * 8 * 4);
-        if (e == cudaSuccess) e = cudaMalloc(&h->p32, K * 4 * 2);
-        if (e == cudaSuccess) e = cudaMalloc(&h->ints, 16 * sizeof(int));
-        if (e == cudaSuccess) e = cudaMalloc(&h->summary, 16 * 8);
-        if (e == cudaSuccess) e = cudaMalloc(&h->bounds, 4 * 8);
-        if (e == cudaSuccess) e = cudaMalloc(&h->scan_i64, K * 8 * 3);
-        if (e == cudaSuccess) e = cudaMalloc(&h->scan_u8, K * 4);
-        if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
-        if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
-        if (e != cudaSuccess) {
-            rc = fail(RL_ECUDA, "rl_instance_create: %s", cudaGetErrorString(e));
-            break;
-        }
-        if ((rc = ensure_trace(h, 1024, 4)))
-            break;
+    int rc = alloc_instance(h);
+    if (!rc) {
         const int64_t *cost[6] = {setup_m, setup_r, hold_m, hold_r, unit_m, unit_r};
         rc = upload(h, demand, returns, cost);
-    } while (0);
-    if (rc) {
-        std::string keep = g_err;
-        rl_instance_destroy(h);
-        g_err = keep;
-        return rc;
     }
-    *out = h;
-    return 0;
+    return finish_create(h, rc, out);
 }
 
 extern "C" int rl_instance_update(rl_instance *h, const int64_t *demand, const int64_t *returns,
@@ -1807,6 +1821,7 @@ extern "C" int rl_int_peak(double *ops_per_s)
 }
 
 #include "gvns_impl.cuh"
+#include "generator.cuh"
 
 extern "C" int64_t rl_launch_count(const rl_instance *h) { return h ? h->launches : 0; }
 

@@ -22,10 +22,17 @@ struct SeedSeq {
     __host__ __device__ static void key(uint64_t seed, uint64_t round, uint64_t worker,
                                         uint64_t out[2])
     {
+        const uint64_t vals[3] = {seed, round, worker};
+        key_n(vals, 3, out);
+    }
+
+    // SeedSequence(vals[0]) (nv = 1) or SeedSequence(tuple(vals)): each value
+    // contributes its little-endian uint32 words (one 0 word for 0)
+    __host__ __device__ static void key_n(const uint64_t *vals, int nv, uint64_t out[2])
+    {
         uint32_t ent[8];
         int n = 0;
-        const uint64_t vals[3] = {seed, round, worker};
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < nv; ++i) {
             uint64_t v = vals[i];
             if (v == 0) {
                 ent[n++] = 0;
