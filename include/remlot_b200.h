@@ -56,9 +56,10 @@ void rl_instance_destroy(rl_instance *h);
 int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uint8_t *sr);
 
 /* Kernel variants of rl_vnd (results are identical; for A/B measurement and
- * tests).  Bit 0: T <= 63 runs two products per warp in lockstep sweeps
- * (default off).  Bit 1: T > 63 never uses one CTA per product (by default
- * a CTA per product is used when K <= 2 x SMs, a warp per product above). */
+ * tests).  Bit 0: reserved (was two products per warp; removed, RL_EINVAL).
+ * Bit 1: T > 63 never uses one CTA per product (by default
+ * a CTA per product is used when K <= 2 x SMs, a warp per product above).
+ * Bits 2/3: T <= 63 slack skip always / never (default: per launch). */
 int rl_instance_set_variant(rl_instance *h, int packed);
 /* info[0..5] = K, T, bytes per period value (4|8), bytes per cost (4|8),
  * SM count, warps per CTA of the resident VND kernel. */
@@ -112,6 +113,11 @@ int rl_vnd_device(rl_instance *h, int k_max, const uint8_t *d_sm_in, const uint8
                   uint8_t *d_sm_out, uint8_t *d_sr_out, void *stream);
 int rl_vnd_collect(rl_instance *h, int64_t *trace, int64_t trace_cap, int64_t *n_trace,
                    int64_t *stats);
+
+/* Per-product results of the last descent on h (K entries each): own
+ * sweeps, moves applied and candidate evaluations performed.  Diagnostic
+ * (work distribution); no reference counterpart. */
+int rl_vnd_product_stats(rl_instance *h, int32_t *sweeps, int32_t *moves, int64_t *evals);
 
 /* rl_instance_update + rl_vnd in one call (same arguments and results): the
  * host->device copies of the instance and plan rows are cut into product

@@ -23,6 +23,7 @@ EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_instance_set_variant",
            "rl_instance_info", "rl_product_costs", "rl_scan_products", "rl_apply_scan",
            "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect", "rl_vnd_host",
+           "rl_vnd_product_stats",
            "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_oracle_optimal", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
            "rl_gvns_round", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
            "rl_rng_probe", "rl_launch_count", "rl_generate_instance", "rl_instance_download",
@@ -61,6 +62,7 @@ def load():
         "rl_vnd": (I, [P, I, P, P, P, P, P, I64, P, P]),
         "rl_vnd_device": (I, [P, I, P, P, P, P, P]),
         "rl_vnd_collect": (I, [P, P, I64, P, P]),
+        "rl_vnd_product_stats": (I, [P, P, P, P]),
         "rl_vnd_host": (I, [P, I] + [P] * 12 + [P, I64, P, P]),
         "rl_initial_solution": (I, [P, P, P]),
         "rl_initial_solution_device": (I, [P, P, P, P]),
@@ -233,6 +235,15 @@ class DeviceInstance:
                      evals=int(st[3]), evals_reference=int(st[4]), moves=int(st[5]),
                      products=int(st[6]), kernel_ns=int(st[7]), ntot_sum=int(st[8]))
         return out_m, out_r, trace[:nt[0]].copy(), stats
+
+    def product_stats(self):
+        """Per-product (sweeps, moves, evals) of the last descent."""
+        sw = np.zeros(self.K, np.int32)
+        mv = np.zeros(self.K, np.int32)
+        ev = np.zeros(self.K, np.int64)
+        check(load().rl_vnd_product_stats(self.h, ptr(sw), ptr(mv), ptr(ev)),
+              "rl_vnd_product_stats")
+        return sw, mv, ev
 
     def vnd_host(self, inst, sm, sr, k_max=4, trace_cap=None):
         """update(inst) + vnd(sm, sr) in one pipelined call (rl_vnd_host)."""

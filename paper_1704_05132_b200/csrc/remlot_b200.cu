@@ -69,7 +69,7 @@ struct InstView {
 };
 
 template <typename C>
-__device__ inline ProductCosts<C> load_costs(const int64_t *c6, int64_t K, int64_t k)
+__device__ inline ProductCosts<C> load_costs(const int64_t *c6, int64_t K, int64_t k, int T)
 {
     ProductCosts<C> p;
     p.km = C(c6[k]);
@@ -78,6 +78,8 @@ __device__ inline ProductCosts<C> load_costs(const int64_t *c6, int64_t K, int64
     p.hr = C(c6[3 * K + k]);
     p.pm = C(c6[4 * K + k]);
     p.pr = C(c6[5 * K + k]);
+    p.a0 = p.pm + C(T) * p.hm;            // wrapping is exact
+    p.b0 = p.pr - p.pm - C(T) * p.hr;
     return p;
 }
 
@@ -160,7 +162,7 @@ __device__ inline C load_product(const Slot<V, C> &s, const InstView<V> &in, con
                                  ProductCosts<C> &pc, Mask &mk)
 {
     stage_begin(s, in, k, lane);
-    pc = load_costs<C>(in.cost6, in.K, k);
+    pc = load_costs<C>(in.cost6, in.K, k, in.T);
     mk = load_rows(s, Mask{}, sm, sr, k, in.T, lane);
     stage_end(s, in, k, lane, phase);
     return build_prefix(s, in.T, pc, lane);
@@ -349,20 +351,18 @@ __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstVie
     if (lane == 0)
         k = o.k_lo + atomicAdd(o.queue, 1);
     k = __shfl_sync(FULL, k, 0);
-    if (k < o.k_hi)
-        stage_begin(s, in, k, lane);
     while (k < o.k_hi) {
-        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k);
+        // the stage aliases xc (free between products): no prefetch; the
+        // copy's latency is hidden by the other resident warps
+        stage_begin(s, in, k, lane);
+        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k, in.T);
         Mask mk = load_rows(s, Mask{}, sm_in, sr_in, k, T, lane);
         stage_end(s, in, k, lane, phase);
         const C K0 = build_prefix(s, T, pc, lane);
-        // prefetch the next product's rows into the (now consumed) stage
         int64_t next = 0;
         if (lane == 0)
             next = o.k_lo + atomicAdd(o.queue, 1);
         next = __shfl_sync(FULL, next, 0);
-        if (next < o.k_hi)
-            stage_begin(s, in, next, lane);
 
         C S, S0;
         VndStats st;
@@ -409,13 +409,12 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
     }
     __syncthreads();
     uint32_t phase = 0;
-    if (warp == 0 && sh_k < o.k_hi)
-        stage_begin(s, in, sh_k, lane);
     while (sh_k < o.k_hi) {
         const int64_t k = sh_k;
-        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k);
+        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k, in.T);
         C K0 = 0;
         if (warp == 0) {
+            stage_begin(s, in, k, lane);   // stage aliases xc: no prefetch
             load_rows(s, MaskSmem{}, sm_in, sr_in, k, T, lane);
             stage_end(s, in, k, lane, phase);
             K0 = build_prefix(s, T, pc, lane);
@@ -423,8 +422,6 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
             if (lane == 0)
                 nx = o.k_lo + atomicAdd(o.queue, 1);
             nx = __shfl_sync(FULL, nx, 0);
-            if (nx < o.k_hi)
-                stage_begin(s, in, nx, lane);
             C S;
             const bool f = base_pass<V, C, MaskSmem, false>(s, mk, T, pc, lane, S);
             if (lane == 0) {
@@ -521,7 +518,6 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
     }
 }
 
-#include "vnd_packed.cuh"
 
 // Totals (one block).  summary: 0 final, 1 start, 2 sweeps, 3 evals done,
 // 4 reference-equivalent evals, 5 moves, 6 K, 8 overflow, 9 sum of decreases.
@@ -747,8 +743,7 @@ struct rl_instance {
     struct GvnsState *gv = nullptr;        // device GVNS state (gvns_impl.cuh)
     double cost_bound = 0.0;               // upper bound of any plan's cost (upload)
     bool cta_long = true;                  // T > 63, few products: CTA per product (k_vnd_cta)
-    bool pack2 = false;                    // T <= 63: two products per warp (vnd_packed.cuh;
-                                           // measured slower, kept for A/B)
+    int skip_mode = 0;                     // slack skip: 0 auto, 1 always, 2 never (A/B)
 };
 
 struct GvnsState;
@@ -975,28 +970,13 @@ static int launch_cfg_cta(rl_instance *h, const void *fn, int64_t nprod, int &gr
     return 0;
 }
 
-template <typename V, typename C>
-static int launch_cfg_pack2(rl_instance *h, const void *fn, int64_t nprod, int &grid, size_t &smem)
-{
-    smem = kWarpsPerCta * 2 * slot_bytes<V, C>(h->T);
-    if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem));
-    if (occ < 1)
-        return fail(RL_EINVAL, "T=%d needs %zu B shared memory per CTA", h->T, smem);
-    const int64_t want = (nprod + 2 * kWarpsPerCta - 1) / (2 * kWarpsPerCta);
-    const int64_t cap = (int64_t)h->sms * occ;
-    grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
-    return 0;
-}
-
 extern "C" int rl_instance_set_variant(rl_instance *h, int packed)
 {
-    if (!h || packed < 0 || packed > 3)
+    // bit 0 (two products per warp) was removed: measured slower
+    if (!h || packed < 0 || packed > 11 || (packed & 12) == 12 || (packed & 1))
         return fail(RL_EINVAL, "rl_instance_set_variant: bad arguments");
-    h->pack2 = (packed & 1) != 0;
     h->cta_long = (packed & 2) == 0;
+    h->skip_mode = (packed & 4) ? 1 : (packed & 8) ? 2 : 0;
     return 0;
 }
 
@@ -1219,7 +1199,6 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
     int grid;
     size_t smem;
     const int64_t nprod = hi - lo;
-    const bool pack = std::is_same<Mask, MaskReg>::value && h->pack2;
     // CTA per product only when the launch is latency-bound (few products):
     // at C4 scale one warp per product keeps 2.4x more products in flight
     // and measured 296 ms vs 434 ms
@@ -1227,25 +1206,17 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
                      nprod <= (int64_t)h->sms * 2;
     // skip pays when the launch is latency-bound: fewer products than ~2
     // waves of resident warps (C2, GVNS) -- measured, DESIGN.md section 5
-#ifdef RL_SKIP_ALWAYS
-    const bool skip = std::is_same<Mask, MaskReg>::value;
-#else
-    const bool skip = std::is_same<Mask, MaskReg>::value && nprod < (int64_t)h->sms * 64;
-#endif
-    const void *fn = pack ? (const void *)k_vnd_pack2<V, C>
-                     : cta ? (const void *)k_vnd_cta<V, C>
+    const bool skip = std::is_same<Mask, MaskReg>::value &&
+                      (h->skip_mode == 1 || (h->skip_mode == 0 && nprod < (int64_t)h->sms * 64));
+    const void *fn = cta ? (const void *)k_vnd_cta<V, C>
                      : skip ? (const void *)k_vnd<V, C, Mask, true>
                             : (const void *)k_vnd<V, C, Mask, false>;
-    int rc = pack ? launch_cfg_pack2<V, C>(h, fn, nprod, grid, smem)
-             : cta ? launch_cfg_cta<V, C>(h, fn, nprod, grid, smem)
-                   : launch_cfg<V, C>(h, fn, nprod, grid, smem);
+    int rc = cta ? launch_cfg_cta<V, C>(h, fn, nprod, grid, smem)
+                 : launch_cfg<V, C>(h, fn, nprod, grid, smem);
     if (rc)
         return rc;
     const VndOut o = vnd_out(h, lo, hi, queue);
-    if (pack)
-        k_vnd_pack2<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
-                                                                  sr_out, k_max, o);
-    else if (cta)
+    if (cta)
         k_vnd_cta<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
                                                                 sr_out, k_max, o);
     else if (skip)
@@ -1365,6 +1336,35 @@ extern "C" int rl_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uin
     CK(cudaMemcpyAsync(sm_out, h->plan + 2 * kt, kt, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(sr_out, h->plan + 3 * kt, kt, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    return 0;
+}
+
+#ifdef RL_WALK_STATS
+extern "C" int rl_walk_stats(int64_t *out, int reset)
+{
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpyFromSymbol(out, g_walk_stats, sizeof(g_walk_stats)));
+    if (reset) {
+        static const unsigned long long z[136] = {};
+        CK(cudaMemcpyToSymbol(g_walk_stats, z, sizeof z));
+    }
+    return 0;
+}
+#endif
+
+// Per-product results of the last rl_vnd / rl_vnd_device on this handle
+// (diagnostics: work distribution over products).
+extern "C" int rl_vnd_product_stats(rl_instance *h, int32_t *sweeps, int32_t *moves,
+                                    int64_t *evals)
+{
+    (void)cudaGetLastError();
+    if (!h || !sweeps || !moves || !evals)
+        return fail(RL_EINVAL, "rl_vnd_product_stats: bad arguments");
+    CK(cudaSetDevice(h->device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(sweeps, h->p32, h->K * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(moves, h->p32 + h->K, h->K * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(evals, h->p64 + 2 * h->K, h->K * 8, cudaMemcpyDeviceToHost));
     return 0;
 }
 

@@ -4,12 +4,14 @@
 // product").  The product's T-period slice lives in shared memory:
 //
 //   stage[2T]   demand row, returns row (V), landed by a 1-D TMA bulk copy
-//   cd[T+1]     cd[t] = sum_{i<t} D[i]       (V)
-//   cr[T+1]     cr[t] = sum_{i<t} R[i]       (V)
-//   xin[T]      cumulative remanufactured quantity entering setup u (V)
+//               into the xc area (consumed by the prefix sums before xc is built)
+//   dr[T+1]     {cd[t], cr[t+1]}: cd[t] = sum_{i<t} D[i], cr[t+1] = sum_{i<=t} R[i]
+//               (V pairs: one 8/16-byte load gives a segment's demand prefix
+//               and the returns available at its setup)
+//   xc[T]       {cpre[u], xin[u]} at setups u: sum of segment costs before u
+//               (C) and cumulative remanufactured quantity entering u (V)
 //   slk[T]      remanufacturing slack CR[u] - xin[u] - seg(u) at sR setups (V)
-//   lm[17]      T <= 63: masks of sR setups with slack < 2^j (j < 16), slack < 0
-//   cpre[T]     sum of segment costs before setup u (C)
+//   lm[18]      T <= 63: masks of sR setups with slack < 2^j (j < 16), all sR, slack < 0
 //   bm[NW],br[NW]  setup bit rows (uint32 words; used when T > 64)
 //   mv[2T+2]    compacted move slots of the current neighborhood (uint16)
 //
@@ -46,19 +48,41 @@ namespace rl {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifdef RL_WALK_STATS
+// Diagnostic build only (tools/walk_stats.py): [0] passes, [1] loop
+// iterations, [2] moves, [3] walk steps, [4] sum of per-pass longest walk,
+// [5] sum of per-pass busiest lane's steps, [8..71] walk-length histogram,
+// [72..135] per-pass iterations histogram (both clamped to 63).
+__device__ unsigned long long g_walk_stats[136];
+#endif
+
 template <typename V> struct VInf;
 template <> struct VInf<int32_t> { static constexpr int32_t value = 1 << 29; };
 template <> struct VInf<int64_t> { static constexpr int64_t value = (int64_t)1 << 61; };
 
+// a0 = p_M + T h_M, b0 = p_R - p_M - T h_R: a segment [u, v) costs
+// seg (a0 - u h_M) + x_R (b0 + u h_R) plus its setup charges (seg_cost)
 template <typename C>
 struct ProductCosts {
-    C km, kr, hm, hr, pm, pr;
+    C km, kr, hm, hr, pm, pr, a0, b0;
+};
+
+template <typename V>
+struct alignas(2 * sizeof(V)) DR {
+    V d, r;   // cd[t], cr[t+1]
+};
+
+template <typename V, typename C>
+struct alignas(2 * sizeof(C)) XC {
+    C c;      // cpre[u]
+    V x;      // xin[u]
 };
 
 template <typename V, typename C>
 struct Slot {
-    V *stage, *cd, *cr, *xin, *slk;
-    C *cpre;
+    V *stage, *slk;
+    DR<V> *dr;
+    XC<V, C> *xc;
     int16_t *nx, *pv;   // T > 63: next setup >= t / last setup < t of the base plan
     uint32_t *bm, *br;
     uint16_t *mv;
@@ -66,11 +90,11 @@ struct Slot {
     uint64_t *bar;
 };
 
-constexpr int kSlackLevels = 16;
+constexpr int kSlackLevels = 16;   // lm[j] = slack < 2^j (j < 16), lm[16] = all sR, lm[17] = slack < 0
 // The slack-level skip (scan_pass) shortens long delta walks, which pays
 // when the descent is latency-bound (few products per SM, GVNS tasks) and
 // costs ~7% extra instructions when it is throughput-bound; the host picks
-// per launch.   // lm[j] = {sR setups: slack < 2^j}, lm[16] = {slack < 0}
+// per launch.
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -79,16 +103,13 @@ __host__ __device__ inline size_t slot_bytes(int T)
 {
     const int NW = (T + 31) >> 5;
     size_t b = 0;
-    b += align16(2 * (size_t)T * sizeof(V));     // stage
-    b += align16((size_t)(T + 1) * sizeof(V));   // cd
-    b += align16((size_t)(T + 1) * sizeof(V));   // cr
-    b += align16((size_t)T * sizeof(V));         // xin
+    b += align16((size_t)(T + 1) * sizeof(DR<V>));      // dr
+    b += align16((size_t)T * sizeof(XC<V, C>));         // xc
     b += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));   // slk (register-mask path only)
-    b += align16((size_t)T * sizeof(C));         // cpre
     b += 2 * align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));   // nx, pv
     b += align16(2 * (size_t)NW * sizeof(uint32_t));
     b += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
-    b += align16((kSlackLevels + 1) * 8);        // lm
+    b += align16((kSlackLevels + 2) * 8);        // lm
     b += 16;                                     // mbarrier
     return b;
 }
@@ -99,18 +120,19 @@ __device__ inline Slot<V, C> carve(unsigned char *base, int T)
     const int NW = (T + 31) >> 5;
     Slot<V, C> s;
     unsigned char *p = base;
-    s.stage = (V *)p; p += align16(2 * (size_t)T * sizeof(V));
-    s.cd = (V *)p;    p += align16((size_t)(T + 1) * sizeof(V));
-    s.cr = (V *)p;    p += align16((size_t)(T + 1) * sizeof(V));
-    s.xin = (V *)p;   p += align16((size_t)T * sizeof(V));
+    s.dr = (DR<V> *)p; p += align16((size_t)(T + 1) * sizeof(DR<V>));
+    s.xc = (XC<V, C> *)p; p += align16((size_t)T * sizeof(XC<V, C>));
+    // the staged demand/returns rows (2T x V <= T x sizeof(XC)) are consumed
+    // by build_prefix before base_pass first writes xc
+    s.stage = (V *)s.xc;
+    static_assert(sizeof(XC<V, C>) >= 2 * sizeof(V), "stage must fit in xc");
     s.slk = (V *)p;   p += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));
-    s.cpre = (C *)p;  p += align16((size_t)T * sizeof(C));
     s.nx = (int16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));
     s.pv = (int16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));
     s.bm = (uint32_t *)p;
     s.br = s.bm + NW; p += align16(2 * (size_t)NW * sizeof(uint32_t));
     s.mv = (uint16_t *)p; p += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
-    s.lm = (uint64_t *)p; p += align16((kSlackLevels + 1) * 8);
+    s.lm = (uint64_t *)p; p += align16((kSlackLevels + 2) * 8);
     s.bar = (uint64_t *)p;
     return s;
 }
@@ -165,6 +187,13 @@ __device__ inline void stage_issue(V *stage, const V *dem, const V *ret, int64_t
 
 template <typename V>
 __device__ inline V vmin(V a, V b) { return a < b ? a : b; }
+
+// smallest j with 2^j >= x (0 for x <= 1)
+__device__ inline int ceil_log2(int32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
+__device__ inline int ceil_log2(int64_t x)
+{
+    return x <= 1 ? 0 : 64 - __clzll((long long)(x - 1));
+}
 
 // ------------------------------------------------------------- bit rows
 
@@ -279,6 +308,7 @@ struct MaskReg {
         return x + __ffsll((long long)(S >> x)) - 1;
     }
     __device__ uint64_t sentinel() const { return 1ull << T; }
+    __device__ static uint64_t sentinel_of(int T) { return 1ull << T; }
     __device__ int next(int x) const { return next_of(M | R | sentinel(), x, T); }
     __device__ uint64_t R_mask() const { return R; }
     __device__ int prev(int x) const
@@ -374,21 +404,22 @@ __device__ inline void store_rows(const Mask &mk, uint8_t *sm, uint8_t *sr, int6
     }
 }
 
-// Cost of one segment [u, v) entered with cumulative remanufacturing X.
-// Follows _kernels.py:66-95 (seg :70-72, avail :73, x_r :74-76, x_m and
-// infeasibility :77-82, setup :83-86, unit :87, holding :88-95 summed).
+// Cost of one segment [u, v) entered with cumulative remanufacturing X, from
+// cdu = cd[u], cru = cr[u+1], cdv = cd[v].  Follows _kernels.py:66-95 (seg
+// :70-72, avail :73, x_r :74-76, x_m and infeasibility :77-82, setup :83-86,
+// unit :87, holding :88-95 summed): p_M x_M + p_R x_R + (T-u)(h_M seg - h_R
+// x_R) regrouped as seg (a0 - u h_M) + x_R (b0 + u h_R).
 template <typename V, typename C>
-__device__ inline bool seg_cost(const V *cd, const V *cr, int T, int u, int v, bool m, bool r,
-                                V X, const ProductCosts<C> &pc, C &c, V &xr)
+__device__ inline bool seg_cost(V cdu, V cru, V cdv, int u, bool m, bool r, V X,
+                                const ProductCosts<C> &pc, C &c, V &xr)
 {
-    RL_ASSERT(0 <= u && u < v && v <= T);
-    const V seg = cd[v] - cd[u];
-    const V avail = cr[u + 1] - X;
+    const V seg = cdv - cdu;
+    const V avail = cru - X;
     xr = r ? vmin(seg, avail) : V(0);
     const V xm = seg - xr;
     // computed unconditionally (no branch): callers discard c when infeasible
-    c = (xr > 0 ? pc.kr : C(0)) + (xm > 0 ? pc.km : C(0)) + pc.pr * C(xr) + pc.pm * C(xm) +
-        C(T - u) * (pc.hm * C(seg) - pc.hr * C(xr));
+    c = (xr > 0 ? pc.kr : C(0)) + (xm > 0 ? pc.km : C(0)) + C(seg) * (pc.a0 - C(u) * pc.hm) +
+        C(xr) * (pc.b0 + C(u) * pc.hr);
     return !(xm > 0 && !m);
 }
 
@@ -401,8 +432,8 @@ __device__ inline C build_prefix(const Slot<V, C> &s, int T, const ProductCosts<
     V carry_d = 0, carry_r = 0;
     C sum_cd = 0, sum_cr = 0;   // sum_t CD[t], sum_t CR[t] (inclusive prefixes)
     if (lane == 0) {
-        s.cd[0] = 0;
-        s.cr[0] = 0;
+        s.dr[0].d = 0;
+        s.dr[T].r = 0;   // cr[T+1]: never used, kept defined
     }
     for (int base = 0; base < T; base += 32) {
         const int t = base + lane;
@@ -419,8 +450,8 @@ __device__ inline C build_prefix(const Slot<V, C> &s, int T, const ProductCosts<
         d += carry_d;
         r += carry_r;
         if (t < T) {
-            s.cd[t + 1] = d;
-            s.cr[t + 1] = r;
+            s.dr[t + 1].d = d;
+            s.dr[t].r = r;
             sum_cd += C(d);
             sum_cr += C(r);
         }
@@ -469,9 +500,10 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
         if (!mk.r(u))
             continue;   // only remanufacturing setups move X
         const int v = mk.next(u + 1);
-        const V seg = s.cd[v] - s.cd[u];
+        const DR<V> e = s.dr[u];
+        const V seg = s.dr[v].d - e.d;
         A += seg;
-        B = vmin<V>(B + seg, s.cr[u + 1]);
+        B = vmin<V>(B + seg, e.r);
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -494,13 +526,15 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
         if (!(m | r))
             continue;
         const int v = mk.next(u + 1);
-        s.xin[u] = X;
-        s.cpre[u] = local;
+        const DR<V> e = s.dr[u];
+        const V cdv = s.dr[v].d;
+        s.xc[u].x = X;
+        s.xc[u].c = local;
         if (kSkip && r)
-            s.slk[u] = s.cr[u + 1] - X - (s.cd[v] - s.cd[u]);
+            s.slk[u] = e.r - X - (cdv - e.d);
         C c;
         V xr;
-        ok &= seg_cost<V, C>(s.cd, s.cr, T, u, v, m, r, X, pc, c, xr);
+        ok &= seg_cost<V, C>(e.d, e.r, cdv, u, m, r, X, pc, c, xr);
         local += c;
         X += xr;
     }
@@ -515,10 +549,10 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
     if (excl != C(0))
         for (int u = lo; u < hi; ++u)
             if (mk.m(u) | mk.r(u))
-                s.cpre[u] += excl;
+                s.xc[u].c += excl;
     S = __shfl_sync(FULL, incl, 31);
     const int f = mk.next(0);
-    ok = ok && s.cd[f] == 0;   // demand before the first setup (_kernels.py:58-60)
+    ok = ok && s.dr[f].d == 0;   // demand before the first setup (_kernels.py:58-60)
     const bool feas = __all_sync(FULL, ok);
     if (kSkip) {
         // slack-level masks for the delta-walk skip (scan_pass): lane l owns
@@ -528,14 +562,19 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
         const V s1 = lane + 32 < T ? s.slk[lane + 32] : INF;
         uint64_t mine = 0;
 #pragma unroll
-        for (int j = 0; j <= kSlackLevels; ++j) {
+        for (int j = 0; j <= kSlackLevels + 1; ++j) {
+            if (j == kSlackLevels) {
+                if (lane == j)
+                    mine = mk.R_mask();   // any delta >= 2^16: every sR setup
+                continue;
+            }
             const V lim = j < kSlackLevels ? (V(1) << j) : V(0);
             const uint64_t mk2 = (uint64_t)__ballot_sync(FULL, s0 < lim) |
                                  ((uint64_t)__ballot_sync(FULL, s1 < lim) << 32);
             if (lane == j)
                 mine = mk2;
         }
-        if (lane <= kSlackLevels)
+        if (lane <= kSlackLevels + 1)
             s.lm[lane] = mine;
     }
     __syncwarp();
@@ -601,18 +640,6 @@ struct PassResult {
     bool improved;
     int slot;     // winning canonical slot
     int n_moves;  // candidates scored (list_moves count)
-};
-
-// Per-lane state of one delta walk.  A move rewrites periods a <= b; its
-// cost is the base plan's prefix up to the last setup before a (cpre, xin),
-// the re-walked segments, and -- once past b the walk's X equals the base
-// plan's X at a setup -- the base plan's suffix.
-template <typename V, typename C, typename Mask>
-struct Walk {
-    typename PatchOf<Mask>::type nw;
-    int u, b, slot;
-    V X;
-    C acc;
 };
 
 template <typename V, typename C, typename Mask>
@@ -682,6 +709,11 @@ __device__ inline void warp_argmin(C &best, int &key)
 // Score the moves i = wi, wi + nw, wi + 2 nw, ... (< n) of the current list
 // on this warp (nw warps share a product in the CTA variant); per-lane
 // results in best/key (initialise best = S, key = INT_MAX).
+//
+// Lane state: 0 idle, 1 a move just taken, 2 walking.  A walking lane is at
+// setup u of its candidate plan with entering X, the candidate's segment
+// costs so far in acc, and cd[u], cr[u+1] carried from the previous step
+// (each step loads one {cd, cr} pair and one {cpre, xin} pair).
 template <typename V, typename C, typename Mask, bool Skip = false>
 __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
                                   const ProductCosts<C> &pc, C S, int nbh, int n, int lane,
@@ -689,92 +721,143 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
 {
     const bool dense = nbh <= 2;
     const unsigned lt = (1u << lane) - 1;
-    Walk<V, C, Mask> w;
-    int idx = lane, next = 32;
-    int gi = idx * nw + wi;
-    bool pend = gi < n, act = false;
-    while (__any_sync(FULL, pend | act)) {
-        if (pend) {
-            pend = false;
+    constexpr bool kSkip = Skip && std::is_same<Mask, MaskReg>::value;
+    typename PatchOf<Mask>::type pw{};
+    int u = 0, b = 0, slot = 0;
+    V X = 0, cdu = 0, cru = 0;
+    C acc = 0;
+    int gi = lane * nw + wi;
+    int state = gi < n ? 1 : 0;
+    int next = 32;   // move indices handed out so far (in units of this warp's share)
+#ifdef RL_WALK_STATS
+    int ws_cur = 0, ws_max = 0, ws_lane = 0, ws_it = 0;
+#endif
+    for (;;) {
+#ifdef RL_WALK_STATS
+        ++ws_it;
+        if (state == 1 && ws_cur) {
+            atomicAdd(&g_walk_stats[8 + min(ws_cur, 63)], 1ull);
+            ws_max = max(ws_max, ws_cur);
+            ws_cur = 0;
+        }
+#endif
+        if (state == 1) {
             RL_ASSERT(gi < n && gi < 4 * T);
-            w.slot = dense ? gi : s.mv[gi];
-            const MoveDesc d = slot_move(mk, nbh, w.slot, T);
+            slot = dense ? gi : s.mv[gi];
+            const MoveDesc d = slot_move(mk, nbh, slot, T);
             int a;
-            w.nw = patch_of<V, C, Mask>(mk, d, a, w.b);
+            pw = patch_of<V, C, Mask>(mk, d, a, b);
             const int p = mk.prev(a);
-            const int pp = p < 0 ? 0 : p;
-            const int u0 = p < 0 ? w.nw.next(0) : p;
-            w.u = u0;
-            w.acc = p < 0 ? C(0) : s.cpre[pp];
-            w.X = p < 0 ? V(0) : s.xin[pp];
-            // no setup before the move: demand ahead of the first setup is infeasible
-            act = p >= 0 || s.cd[u0] == 0;
-            if (act && u0 >= T) {   // no setup at all and no demand: cost 0
-                act = false;
-                if (w.acc < best) {
-                    best = w.acc;
-                    key = w.slot;
+            if (p >= 0) {   // the prefix before p is the base plan's
+                const XC<V, C> e = s.xc[p];
+                u = p;
+                acc = e.c;
+                X = e.x;
+            } else {
+                u = pw.next(0);
+                acc = 0;
+                X = 0;
+            }
+            const DR<V> e = s.dr[u];
+            cdu = e.d;
+            cru = e.r;
+            // no setup before the move: demand ahead of the first setup is
+            // infeasible; no setup at all and no demand: cost 0
+            state = (p >= 0 || cdu == 0) ? 2 : 0;
+            if (state == 2 && u >= T) {
+                state = 0;
+                if (acc < best) {
+                    best = acc;
+                    key = slot;
                 }
             }
         }
-        if (act) {
-            int u = w.u;
-            bool done = false;
-            if (Skip && std::is_same<Mask, MaskReg>::value) {
-                // Past the move (u > b) the rows equal the base plan's and
-                // only the entering X differs (delta != 0).  A segment then
-                // costs what it costs in the base plan unless it starts at an
-                // sR setup whose slack < max(delta, 0) (its min(seg, avail)
-                // changes).  Jump to the next setup in the slack-level mask
-                // that bounds that set (false positives are merely evaluated
-                // exactly) and add the base cost of the skipped segments.
-                const bool ph2 = u > w.b;
-                const V delta = w.X - s.xin[u];
-                const int j = delta <= 1 ? 0 : 64 - __clzll((long long)(uint64_t)(delta - 1));
-                const uint64_t cand = (delta < 0 ? s.lm[kSlackLevels]
-                                       : j < kSlackLevels ? s.lm[j] : mk.R_mask()) | (1ull << T);
-                const int q = ph2 ? MaskReg::next_of(cand, u, T) : u;
-                const int qq = q < T ? q : u;
-                const C skipped = (q < T ? s.cpre[qq] : S) - s.cpre[u];
-                if (ph2) {
-                    w.acc += skipped;
-                    w.X = s.xin[qq] + delta;
-                }
-                done = q >= T;
-                u = qq;
-            }
+        if (state == 2) {
+#ifdef RL_WALK_STATS
+            ++ws_cur;
+            ++ws_lane;
+#endif
             // one segment of the walk, branch-free (every busy lane issues the
             // same instructions): cost, resync test, finish, argmin update
-            const int v = w.nw.next(u + 1);
+            const int v = pw.next(u + 1);
+            const DR<V> ev = s.dr[v];
             C c;
             V xr;
-            const bool ok = seg_cost<V, C>(s.cd, s.cr, T, u, v, w.nw.m(u), w.nw.r(u), w.X, pc, c,
-                                           xr);
-            const int vv = v < T ? v : T - 1;
-            const V xv = s.xin[vv];
-            const C cv = s.cpre[vv];
-            const C acc = done ? w.acc : w.acc + c;
-            const V X = w.X + xr;
-            const bool sync = !done && v < T && v > w.b && X == xv;
-            const bool fin = done || v >= T || sync;
-            const C total = sync ? acc + (S - cv) : acc;
-            const bool take = (done || ok) && fin && total < best;
+            const bool ok = seg_cost<V, C>(cdu, cru, ev.d, u, pw.m(u), pw.r(u), X, pc, c, xr);
+            const XC<V, C> bv = s.xc[v < T ? v : T - 1];
+            acc += c;
+            X += xr;
+            // past the move the rows equal the base plan's; only X may differ
+            const bool past = v < T && v > b;
+            bool sync;
+            C total;
+            if constexpr (kSkip) {
+                // Slack skip: with X = base + delta at v, a later segment costs
+                // what it costs in the base plan unless it starts at an sR setup
+                // whose slack < max(delta, 0) (for delta < 0: slack < 0), where
+                // min(seg, avail) changes.  Jump to the next setup of the
+                // slack-level mask bounding that set (false positives are just
+                // walked exactly), adding the base cost of the segments skipped;
+                // no such setup left = the rest of the base plan (resync).
+                const V delta = X - bv.x;
+                const int li = delta < 0 ? kSlackLevels + 1 : min(ceil_log2(delta), kSlackLevels);
+                const int q = MaskReg::next_of(s.lm[li] | MaskReg::sentinel_of(T), v, T);
+                sync = past && (delta == 0 || q >= T);
+                total = acc + (S - bv.c);
+                const int qq = past && q < T ? q : v;
+                const XC<V, C> bq = s.xc[qq < T ? qq : T - 1];
+                const DR<V> eq = s.dr[qq];
+                acc += bq.c - bv.c;   // 0 unless past (qq == v otherwise)
+                X = past ? bq.x + delta : X;
+                u = qq;
+                cdu = eq.d;
+                cru = eq.r;
+            } else {
+                sync = past && X == bv.x;
+                total = acc + (S - bv.c);
+                u = v;
+                cdu = ev.d;
+                cru = ev.r;
+            }
+            const bool fin = v >= T || sync;
+            total = sync ? total : acc;
+            const bool take = ok && fin && total < best;
             best = take ? total : best;
-            key = take ? w.slot : key;
-            act = !done && ok && !fin;
-            w.acc = acc;
-            w.X = X;
-            w.u = v;
+            key = take ? slot : key;
+            state = ok && !fin ? 2 : 0;
         }
-        const bool idle = !(pend | act);
-        const unsigned m = __ballot_sync(FULL, idle);
-        if (idle) {
-            idx = next + __popc(m & lt);
-            gi = idx * nw + wi;
-            pend = gi < n;
+        const unsigned m = __ballot_sync(FULL, state == 0);
+        const bool more = m != FULL || next * nw + wi < n;
+        if (state == 0) {
+            gi = (next + __popc(m & lt)) * nw + wi;
+            state = gi < n ? 1 : 0;
         }
         next += __popc(m);
+        if (!more)
+            break;
     }
+#ifdef RL_WALK_STATS
+    if (ws_cur) {
+        atomicAdd(&g_walk_stats[8 + min(ws_cur, 63)], 1ull);
+        ws_max = max(ws_max, ws_cur);
+    }
+    int tot = ws_lane, mx = ws_max, busy = ws_lane;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        tot += __shfl_xor_sync(FULL, tot, off);
+        mx = max(mx, __shfl_xor_sync(FULL, mx, off));
+        busy = max(busy, __shfl_xor_sync(FULL, busy, off));
+    }
+    if (lane == 0) {
+        atomicAdd(&g_walk_stats[0], 1ull);
+        atomicAdd(&g_walk_stats[1], (unsigned long long)ws_it);
+        atomicAdd(&g_walk_stats[2], (unsigned long long)n);
+        atomicAdd(&g_walk_stats[3], (unsigned long long)tot);
+        atomicAdd(&g_walk_stats[4], (unsigned long long)mx);
+        atomicAdd(&g_walk_stats[5], (unsigned long long)busy);
+        atomicAdd(&g_walk_stats[72 + min(ws_it, 63)], 1ull);
+    }
+#endif
 }
 
 template <typename V, typename C, typename Mask, bool Skip = false>
