@@ -318,16 +318,22 @@ struct VndOut {
 // and runs that product's VND to its own fixpoint (global VND decomposes
 // exactly per product), logging each pass's decrease
 // into trace_dec[sweep * k_max + nbh - 1] with exact int64 atomics so the
-// reference's lockstep trace is reproduced.  The next product's rows are
-// prefetched by TMA while the current one is processed.
-// CTAs per SM the register allocation must allow (register-light int32 /
-// register-mask variant runs 6 x 4 warps per SM; measured).
+// reference's lockstep trace is reproduced.  A product's rows are staged by
+// TMA into the warp's (then free) xc area.
+// CTAs per SM the register allocation must allow (measured):
+// int32 register-mask variant 7 x 4 warps per SM; shared-memory-mask
+// variants 6 (int32 costs) and 4 (int64 costs: 13.9 KB shared per warp at
+// T = 520 allows no more).
 template <typename V, typename C, typename Mask> struct VndMinBlocks { static constexpr int value = 1; };
 template <> struct VndMinBlocks<int32_t, int32_t, MaskReg> { static constexpr int value = 7; };
 #ifndef RL_SMEM_MINB
-#define RL_SMEM_MINB 3
+#define RL_SMEM_MINB 4
+#endif
+#ifndef RL_SMEM32_MINB
+#define RL_SMEM32_MINB 6
 #endif
 template <> struct VndMinBlocks<int32_t, int64_t, MaskSmem> { static constexpr int value = RL_SMEM_MINB; };
+template <> struct VndMinBlocks<int32_t, int32_t, MaskSmem> { static constexpr int value = RL_SMEM32_MINB; };
 #ifdef RL_VND_MINB
 #define RL_VND_MINB_OF(V, C, M) RL_VND_MINB
 #else
@@ -402,7 +408,7 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int T = in.T;
     const Slot<V, C> s = carve<V, C>(smem, T);
-    const MaskSmem mk{s.bm, s.br, s.nx, s.pv, T};
+    const MaskSmem mk{s.bm, s.br, s.nx, T};
     if (threadIdx.x == 0) {
         mbar_init(s.bar);
         sh_k = o.k_lo + atomicAdd(o.queue, 1);

@@ -78,12 +78,59 @@ struct alignas(2 * sizeof(C)) XC {
     V x;      // xin[u]
 };
 
+// {cpre, xin} per period: one interleaved array when both have the same
+// width (one 8/16-byte load per query), two arrays for int32 X with int64
+// costs (12 bytes per period instead of a padded 16: the long-horizon
+// kernel's shared memory per warp bounds its occupancy).
+template <typename V, typename C, bool Split = (sizeof(V) != sizeof(C))>
+struct XCStore {
+    XC<V, C> *p;
+    __host__ __device__ static size_t bytes(int T) { return (size_t)T * sizeof(XC<V, C>); }
+    __device__ void carve(unsigned char *b, int) { p = (XC<V, C> *)b; }
+    __device__ XC<V, C> operator[](int i) const { return p[i]; }
+    __device__ void set(int i, V x, C c) const
+    {
+        p[i].x = x;
+        p[i].c = c;
+    }
+    __device__ void add_c(int i, C d) const { p[i].c += d; }
+    __device__ void *base() const { return p; }
+};
+template <typename V, typename C>
+struct XCStore<V, C, true> {
+    C *c;
+    V *x;
+    __host__ __device__ static size_t bytes(int T)
+    {
+        return ((size_t)T * sizeof(C) + 15) / 16 * 16 + (size_t)T * sizeof(V);
+    }
+    __device__ void carve(unsigned char *b, int T)
+    {
+        c = (C *)b;
+        x = (V *)(b + ((size_t)T * sizeof(C) + 15) / 16 * 16);
+    }
+    __device__ XC<V, C> operator[](int i) const
+    {
+        XC<V, C> e;
+        e.c = c[i];
+        e.x = x[i];
+        return e;
+    }
+    __device__ void set(int i, V xv, C cv) const
+    {
+        x[i] = xv;
+        c[i] = cv;
+    }
+    __device__ void add_c(int i, C d) const { c[i] += d; }
+    __device__ void *base() const { return c; }
+};
+
 template <typename V, typename C>
 struct Slot {
     V *stage, *slk;
     DR<V> *dr;
-    XC<V, C> *xc;
-    int16_t *nx, *pv;   // T > 63: next setup >= t / last setup < t of the base plan
+    XCStore<V, C> xc;
+    int16_t *nx;        // T > 63: next setup >= t of the base plan
     uint32_t *bm, *br;
     uint16_t *mv;
     uint64_t *lm;
@@ -104,9 +151,9 @@ __host__ __device__ inline size_t slot_bytes(int T)
     const int NW = (T + 31) >> 5;
     size_t b = 0;
     b += align16((size_t)(T + 1) * sizeof(DR<V>));      // dr
-    b += align16((size_t)T * sizeof(XC<V, C>));         // xc
+    b += align16(XCStore<V, C>::bytes(T));             // xc
     b += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));   // slk (register-mask path only)
-    b += 2 * align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));   // nx, pv
+    b += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));   // nx
     b += align16(2 * (size_t)NW * sizeof(uint32_t));
     b += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
     b += align16((kSlackLevels + 2) * 8);        // lm
@@ -121,14 +168,13 @@ __device__ inline Slot<V, C> carve(unsigned char *base, int T)
     Slot<V, C> s;
     unsigned char *p = base;
     s.dr = (DR<V> *)p; p += align16((size_t)(T + 1) * sizeof(DR<V>));
-    s.xc = (XC<V, C> *)p; p += align16((size_t)T * sizeof(XC<V, C>));
-    // the staged demand/returns rows (2T x V <= T x sizeof(XC)) are consumed
-    // by build_prefix before base_pass first writes xc
-    s.stage = (V *)s.xc;
-    static_assert(sizeof(XC<V, C>) >= 2 * sizeof(V), "stage must fit in xc");
+    s.xc.carve(p, T); p += align16(XCStore<V, C>::bytes(T));
+    // the staged demand/returns rows (2T x V <= the xc area) are consumed by
+    // build_prefix before base_pass first writes xc
+    s.stage = (V *)s.xc.base();
+    static_assert(sizeof(C) + sizeof(V) >= 2 * sizeof(V), "stage must fit in xc");
     s.slk = (V *)p;   p += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));
     s.nx = (int16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));
-    s.pv = (int16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));
     s.bm = (uint32_t *)p;
     s.br = s.bm + NW; p += align16(2 * (size_t)NW * sizeof(uint32_t));
     s.mv = (uint16_t *)p; p += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
@@ -199,12 +245,12 @@ __device__ inline int ceil_log2(int64_t x)
 
 __device__ inline bool wbit(const uint32_t *w, int t) { return (w[t >> 5] >> (t & 31)) & 1u; }
 
-// Setup rows held in shared memory words (T > 63).  Next/previous-setup
-// queries read per-period tables (nx, pv) that base_pass rebuilds whenever
-// the rows change, so they are one shared-memory load each.
+// Setup rows held in shared memory words (T > 63).  Next-setup queries (one
+// per walk step) read a per-period table nx that base_pass rebuilds whenever
+// the rows change; previous-setup queries (one per move) scan the words.
 struct MaskSmem {
     uint32_t *bm, *br;
-    int16_t *nx, *pv;
+    int16_t *nx;
     int T;
     __device__ bool m(int t) const { return wbit(bm, t); }
     __device__ bool r(int t) const { return wbit(br, t); }
@@ -215,11 +261,19 @@ struct MaskSmem {
         RL_ASSERT(x >= 0);
         return x >= T ? T : nx[x];
     }
-    // largest setup period < x (-1 if none); needs fresh tables
+    // largest setup period < x (-1 if none)
     __device__ int prev(int x) const
     {
         RL_ASSERT(x <= T);
-        return x <= 0 ? -1 : pv[x];
+        if (x <= 0)
+            return -1;
+        int w = (x - 1) >> 5;
+        uint32_t bits = (bm[w] | br[w]) & (0xffffffffu >> (31 - ((x - 1) & 31)));
+        while (!bits && w > 0) {
+            --w;
+            bits = bm[w] | br[w];
+        }
+        return bits ? (w << 5) + 31 - __clz(bits) : -1;
     }
     __device__ void set(int t, bool mv, bool rv, int lane)
     {
@@ -231,25 +285,21 @@ struct MaskSmem {
     }
     __device__ void sync() const { __syncwarp(); }
     __device__ uint64_t R_mask() const { return 0; }   // unused (no skip for T > 63)
-    // rebuild nx/pv from the bit rows (lane chunks + warp min/max scans)
+    // rebuild nx from the bit rows (lane chunks + a warp min scan)
     __device__ void build_tables(int lane) const
     {
         const int L = (T + 31) >> 5;
         const int lo = lane * L, hi = min(lo + L, T);
-        int first = T, last = -1;
-        for (int t = lo; t < hi; ++t)
-            if (setup(t)) {
-                first = min(first, t);
-                last = t;
-            }
-        int sf = first, pl = last;
+        int first = T;
+        for (int t = hi - 1; t >= lo; --t)
+            if (setup(t))
+                first = t;
+        int sf = first;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const int o = __shfl_down_sync(FULL, sf, off), q = __shfl_up_sync(FULL, pl, off);
+            const int o = __shfl_down_sync(FULL, sf, off);
             if (lane + off < 32)
                 sf = min(sf, o);
-            if (lane >= off)
-                pl = max(pl, q);
         }
         int run = __shfl_down_sync(FULL, sf, 1);
         if (lane == 31)
@@ -259,18 +309,8 @@ struct MaskSmem {
                 run = t;
             nx[t] = (int16_t)run;
         }
-        run = __shfl_up_sync(FULL, pl, 1);
-        if (lane == 0)
-            run = -1;
-        for (int t = lo; t < hi; ++t) {
-            pv[t] = (int16_t)run;
-            if (setup(t))
-                run = t;
-        }
-        if (lane == 31) {
+        if (lane == 31)
             nx[T] = (int16_t)T;
-            pv[T] = (int16_t)pl;
-        }
         __syncwarp();
     }
 };
@@ -376,7 +416,7 @@ __device__ inline MaskSmem load_rows(const Slot<V, C> &s, MaskSmem, const uint8_
         }
     }
     __syncwarp();
-    return MaskSmem{s.bm, s.br, s.nx, s.pv, T};
+    return MaskSmem{s.bm, s.br, s.nx, T};
 }
 
 template <typename V, typename C>
@@ -528,8 +568,7 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
         const int v = mk.next(u + 1);
         const DR<V> e = s.dr[u];
         const V cdv = s.dr[v].d;
-        s.xc[u].x = X;
-        s.xc[u].c = local;
+        s.xc.set(u, X, local);
         if (kSkip && r)
             s.slk[u] = e.r - X - (cdv - e.d);
         C c;
@@ -549,7 +588,7 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
     if (excl != C(0))
         for (int u = lo; u < hi; ++u)
             if (mk.m(u) | mk.r(u))
-                s.xc[u].c += excl;
+                s.xc.add_c(u, excl);
     S = __shfl_sync(FULL, incl, 31);
     const int f = mk.next(0);
     ok = ok && s.dr[f].d == 0;   // demand before the first setup (_kernels.py:58-60)
