@@ -130,7 +130,7 @@ struct Slot {
     V *stage, *slk;
     DR<V> *dr;
     XCStore<V, C> xc;
-    int16_t *nx;        // T > 63: next setup >= t of the base plan
+    uint16_t *nx;       // T > 63: next setup >= t of the base plan and its kind
     uint32_t *bm, *br;
     uint16_t *mv;
     uint64_t *lm;
@@ -174,7 +174,7 @@ __device__ inline Slot<V, C> carve(unsigned char *base, int T)
     s.stage = (V *)s.xc.base();
     static_assert(sizeof(C) + sizeof(V) >= 2 * sizeof(V), "stage must fit in xc");
     s.slk = (V *)p;   p += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));
-    s.nx = (int16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));
+    s.nx = (uint16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(uint16_t));
     s.bm = (uint32_t *)p;
     s.br = s.bm + NW; p += align16(2 * (size_t)NW * sizeof(uint32_t));
     s.mv = (uint16_t *)p; p += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
@@ -246,11 +246,17 @@ __device__ inline int ceil_log2(int64_t x)
 __device__ inline bool wbit(const uint32_t *w, int t) { return (w[t >> 5] >> (t & 31)) & 1u; }
 
 // Setup rows held in shared memory words (T > 63).  Next-setup queries (one
-// per walk step) read a per-period table nx that base_pass rebuilds whenever
-// the rows change; previous-setup queries (one per move) scan the words.
+// per walk step) read a per-period table that base_pass rebuilds whenever
+// the rows change: nx[t] = first setup >= t (bits 0-13) and its type (bits
+// 14-15: 1 = manufacturing, 2 = remanufacturing), so a walk step learns the
+// next segment's start and setup kind from one 16-bit load.
+// Previous-setup queries (one per move) scan the words.
+constexpr int kTypeShift = 14;
+constexpr int kPeriodMask = (1 << kTypeShift) - 1;   // T <= 16000 < 2^14
+
 struct MaskSmem {
     uint32_t *bm, *br;
-    int16_t *nx;
+    uint16_t *nx;
     int T;
     __device__ bool m(int t) const { return wbit(bm, t); }
     __device__ bool r(int t) const { return wbit(br, t); }
@@ -259,8 +265,10 @@ struct MaskSmem {
     __device__ int next(int x) const
     {
         RL_ASSERT(x >= 0);
-        return x >= T ? T : nx[x];
+        return x >= T ? T : (nx[x] & kPeriodMask);
     }
+    // kind (m | r << 1) of setup period t (t must be a setup); fresh tables
+    __device__ int setup_type(int t) const { return nx[t] >> kTypeShift; }
     // largest setup period < x (-1 if none)
     __device__ int prev(int x) const
     {
@@ -304,34 +312,59 @@ struct MaskSmem {
         int run = __shfl_down_sync(FULL, sf, 1);
         if (lane == 31)
             run = T;
+        // the first setup >= hi (a lane's successor chunk) and its kind
+        int ty = run < T ? (int)m(run) | (int)r(run) << 1 : 0;
         for (int t = hi - 1; t >= lo; --t) {
-            if (setup(t))
+            const int k = (int)m(t) | (int)r(t) << 1;
+            if (k) {
                 run = t;
-            nx[t] = (int16_t)run;
+                ty = k;
+            }
+            nx[t] = (uint16_t)(run | ty << kTypeShift);
         }
         if (lane == 31)
-            nx[T] = (int16_t)T;
+            nx[T] = (uint16_t)T;
         __syncwarp();
     }
 };
 
-// The rows of a candidate move: base rows with periods a <= b rewritten.
+// The rows of a candidate move: base rows with periods a <= b rewritten
+// (ta, tb = the new kinds m | r << 1 there).
 struct PatchedSmem {
     MaskSmem base;
-    int a, b;
-    bool ma, ra, mb, rb;
-    __device__ bool m(int t) const { return t == a ? ma : t == b ? mb : base.m(t); }
-    __device__ bool r(int t) const { return t == a ? ra : t == b ? rb : base.r(t); }
+    int a, b, ta, tb;
+    // first setup >= x (T if none) and its kind
+    __device__ int next_t(int x, int &ty) const
+    {
+        const int T = base.T;
+        int e = x >= T ? T : base.nx[x];
+        int t = e & kPeriodMask;
+        ty = e >> kTypeShift;
+        // base setups the move clears (at most a and b) are skipped
+#pragma unroll 1
+        while (t < T && (t == a || t == b)) {
+            const int pt = t == a ? ta : tb;
+            if (pt) {
+                ty = pt;
+                break;
+            }
+            e = t + 1 >= T ? T : base.nx[t + 1];
+            t = e & kPeriodMask;
+            ty = e >> kTypeShift;
+        }
+        if (x <= a && a < t && ta) {
+            t = a;
+            ty = ta;
+        } else if (x <= b && b < t && tb) {
+            t = b;
+            ty = tb;
+        }
+        return t;
+    }
     __device__ int next(int x) const
     {
-        int t = base.next(x);
-        while (t < base.T && (t == a || t == b) && !(m(t) | r(t)))
-            t = base.next(t + 1);
-        if (x <= a && a < t && (ma | ra))
-            t = a;
-        else if (x <= b && b < t && (mb | rb))
-            t = b;
-        return t;
+        int ty;
+        return next_t(x, ty);
     }
 };
 
@@ -351,6 +384,7 @@ struct MaskReg {
     __device__ static uint64_t sentinel_of(int T) { return 1ull << T; }
     __device__ int next(int x) const { return next_of(M | R | sentinel(), x, T); }
     __device__ uint64_t R_mask() const { return R; }
+    __device__ int setup_type(int t) const { return (int)m(t) | (int)r(t) << 1; }
     __device__ int prev(int x) const
     {
         const uint64_t w = (M | R) & ((1ull << x) - 1);   // x <= T <= 63
@@ -380,6 +414,12 @@ struct PatchedReg {
     // period t is bit 63-t of SR: shifting left by x drops periods < x and
     // the leading one is the first setup >= x (count leading zeros)
     __device__ int next(int x) const { return x + __clzll((long long)(SR << x)); }
+    __device__ int next_t(int x, int &ty) const
+    {
+        const int t = next(x);
+        ty = (int)m(t) | (int)r(t) << 1;   // 0 at the sentinel T
+        return t;
+    }
 };
 
 template <typename Mask> struct PatchOf;
@@ -388,7 +428,7 @@ template <> struct PatchOf<MaskSmem> {
     __device__ static PatchedSmem make(const MaskSmem &b, int a, int bb, bool ma, bool ra,
                                        bool mb, bool rb)
     {
-        return PatchedSmem{b, a, bb, ma, ra, mb, rb};
+        return PatchedSmem{b, a, bb, (int)ma | (int)ra << 1, (int)mb | (int)rb << 1};
     }
 };
 template <> struct PatchOf<MaskReg> {
@@ -761,8 +801,9 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
     const bool dense = nbh <= 2;
     const unsigned lt = (1u << lane) - 1;
     constexpr bool kSkip = Skip && std::is_same<Mask, MaskReg>::value;
+    constexpr bool kRegMask = std::is_same<Mask, MaskReg>::value;
     typename PatchOf<Mask>::type pw{};
-    int u = 0, b = 0, slot = 0;
+    int u = 0, b = 0, slot = 0, tu = 0;   // tu: kind (m | r << 1) of setup u
     V X = 0, cdu = 0, cru = 0;
     C acc = 0;
     int gi = lane * nw + wi;
@@ -790,10 +831,12 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
             if (p >= 0) {   // the prefix before p is the base plan's
                 const XC<V, C> e = s.xc[p];
                 u = p;
+                if (!kRegMask)
+                    tu = mk.setup_type(p);
                 acc = e.c;
                 X = e.x;
             } else {
-                u = pw.next(0);
+                u = kRegMask ? pw.next(0) : pw.next_t(0, tu);
                 acc = 0;
                 X = 0;
             }
@@ -818,11 +861,23 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
 #endif
             // one segment of the walk, branch-free (every busy lane issues the
             // same instructions): cost, resync test, finish, argmin update
-            const int v = pw.next(u + 1);
+            // register masks test the candidate's bits directly (measured
+            // faster); shared-memory masks carry the kind from the nx table
+            int tv = 0, v;
+            bool mu, ru;
+            if constexpr (kRegMask) {
+                v = pw.next(u + 1);
+                mu = pw.m(u);
+                ru = pw.r(u);
+            } else {
+                v = pw.next_t(u + 1, tv);
+                mu = tu & 1;
+                ru = tu >> 1;
+            }
             const DR<V> ev = s.dr[v];
             C c;
             V xr;
-            const bool ok = seg_cost<V, C>(cdu, cru, ev.d, u, pw.m(u), pw.r(u), X, pc, c, xr);
+            const bool ok = seg_cost<V, C>(cdu, cru, ev.d, u, mu, ru, X, pc, c, xr);
             const XC<V, C> bv = s.xc[v < T ? v : T - 1];
             acc += c;
             X += xr;
@@ -855,6 +910,7 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
                 sync = past && X == bv.x;
                 total = acc + (S - bv.c);
                 u = v;
+                tu = tv;
                 cdu = ev.d;
                 cru = ev.r;
             }
