@@ -280,6 +280,13 @@ __device__ inline bool vnd_product(const Slot<V, C> &s, Mask &mk, int T, const P
             C best;
             const PassResult r = scan_pass<V, C, Mask, Skip>(s, mk, T, pc, S, nbh, lane, best);
             st.evals += r.n_moves;
+#ifdef RL_WALK_STATS
+            if (lane == 0) {
+                atomicAdd(&g_walk_stats[136 + nbh], 1ull);
+                atomicAdd(&g_walk_stats[144 + nbh], (unsigned long long)r.improved);
+                atomicAdd(&g_walk_stats[152 + nbh], (unsigned long long)r.n_moves);
+            }
+#endif
             if (r.improved) {
                 apply_slot(mk, nbh, r.slot, T, lane);
                 dirty = true;
@@ -1351,7 +1358,7 @@ extern "C" int rl_walk_stats(int64_t *out, int reset)
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpyFromSymbol(out, g_walk_stats, sizeof(g_walk_stats)));
     if (reset) {
-        static const unsigned long long z[136] = {};
+        static const unsigned long long z[160] = {};
         CK(cudaMemcpyToSymbol(g_walk_stats, z, sizeof z));
     }
     return 0;

@@ -52,8 +52,10 @@ constexpr unsigned FULL = 0xffffffffu;
 // Diagnostic build only (tools/walk_stats.py): [0] passes, [1] loop
 // iterations, [2] moves, [3] walk steps, [4] sum of per-pass longest walk,
 // [5] sum of per-pass busiest lane's steps, [8..71] walk-length histogram,
-// [72..135] per-pass iterations histogram (both clamped to 63).
-__device__ unsigned long long g_walk_stats[136];
+// [72..135] per-pass iterations histogram (both clamped to 63),
+// [136 + nbh] passes, [144 + nbh] improving passes, [152 + nbh] moves of
+// neighborhood nbh (vnd_product).
+__device__ unsigned long long g_walk_stats[160];
 #endif
 
 template <typename V> struct VInf;

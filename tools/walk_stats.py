@@ -21,7 +21,7 @@ from paper_1704_05132_b200._native import DeviceInstance  # noqa: E402
 SIZES = {"c3": (100000, 52), "c2": (1000, 52), "c4": (10000, 520)}
 lib = _native.load()
 lib.rl_walk_stats.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros(136, np.int64)
+buf = np.zeros(160, np.int64)
 variants = [int(v) for v in os.environ.get("RL_VARIANTS", "0").split(",")]
 for name, variant in [(n, v) for n in (sys.argv[1:] or ["c2", "c3"]) for v in variants]:
     K, T = SIZES[name]
@@ -39,6 +39,9 @@ for name, variant in [(n, v) for n in (sys.argv[1:] or ["c2", "c3"]) for v in va
     h = buf[8:72]
     print("  walk-length histogram (len:count%): " +
           " ".join(f"{i}:{100 * h[i] / h.sum():.1f}" for i in range(64) if h[i] * 1000 > h.sum()))
+    print("  per neighborhood (passes, improving fraction, moves/pass): " + "  ".join(
+        f"N{j}: {buf[136 + j]} {buf[144 + j] / max(buf[136 + j], 1):.3f} "
+        f"{buf[152 + j] / max(buf[136 + j], 1):.1f}" for j in range(1, 5)))
     h = buf[72:136]
     print("  iterations/pass histogram: " +
           " ".join(f"{i}:{100 * h[i] / h.sum():.1f}" for i in range(64) if h[i] * 1000 > h.sum()))
