@@ -332,7 +332,10 @@ struct VndOut {
 // variants 6 (int32 costs) and 4 (int64 costs: 13.9 KB shared per warp at
 // T = 520 allows no more).
 template <typename V, typename C, typename Mask> struct VndMinBlocks { static constexpr int value = 1; };
-template <> struct VndMinBlocks<int32_t, int32_t, MaskReg> { static constexpr int value = 7; };
+#ifndef RL_REG_MINB
+#define RL_REG_MINB 7
+#endif
+template <> struct VndMinBlocks<int32_t, int32_t, MaskReg> { static constexpr int value = RL_REG_MINB; };
 #ifndef RL_SMEM_MINB
 #define RL_SMEM_MINB 4
 #endif
