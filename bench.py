@@ -120,6 +120,32 @@ def cpu_reference(inst, sample_products, steps, warmup, threads):
                 sweeps=stats["sweeps"])
 
 
+def hbm_bytes(wl):
+    """Algorithmic HBM bytes of one VND launch per GPU:
+    int32 D, R rows + six int64 cost vectors + plan in/out bytes."""
+    K, T = wl["products"], wl["periods"]
+    return K * (8 * T + 48) + K * 2 * T * 2
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 7700.0   # B200_PROFILING.md fallback
+
+
+def ncu_summary(workload):
+    """Issue-slot / pipe utilisation of k_vnd from the committed ncu --set
+    full capture of this workload (profiles/k_vnd_<workload>_ncu.json)."""
+    path = os.path.join(ROOT, "profiles", f"k_vnd_{workload}_ncu.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
 def traffic_bytes(workload):
     """dram__bytes_read.sum + dram__bytes_write.sum of one k_vnd launch on
     this workload from the committed ncu --set full capture (profiles/), or
@@ -203,11 +229,13 @@ def main():
     K, T = wl["products"], wl["periods"]
     if args.scaling == "weak":
         K *= world
-    inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=0))
     from paper_1704_05132_b200.sharded import shard_bounds
     lo, hi = shard_bounds(K, rank, world)
-    shard = inst.slice(lo, hi)
-    dev = _native.DeviceInstance(shard)
+    # each rank draws only its shard of the seed-0 instance on its device
+    # (rl_generate_instance: bit-identical to generate_instance, tested);
+    # the host copy feeds the e2e leg's pinned uploads
+    dev = _native.DeviceInstance.generate(GeneratorConfig(products=K, periods=T, seed=0), lo, hi)
+    shard = dev.download()
     stream = torch.cuda.Stream()   # a real stream: events and kernels share it
     torch.cuda.set_stream(stream)
     sptr = ctypes.c_void_p(stream.cuda_stream)
@@ -319,9 +347,15 @@ def main():
                          "peak_source": "INT32 add microbenchmark run in this bench",
                          "ops_definition": "8*T int ops per performed neighbor evaluation "
                                            "(SURVEY.md 8(d))",
-                         "kernel_ms": vnd_kernel_ms, "traffic": traffic_bytes(args.workload)},
+                         "kernel_ms": vnd_kernel_ms, "traffic": traffic_bytes(args.workload),
+                         "ncu": ncu_summary(args.workload),
+                         "hbm": {"achieved": hbm_bytes(wl) * world / (vnd_kernel_ms / 1e3) / 1e9,
+                                 "peak": hbm_peak(), "unit": "GB/s",
+                                 "note": "algorithmic bytes (instance + plans once) per "
+                                         "launch / kernel time: not the binding resource"}},
         }
         if world == 1 and not args.no_cpu_baseline:
+            inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=0))
             # bounded sample sized for ~10-20 s of CPU work on this host
             probe = cpu_reference(inst, min(1000, K), 1, 0, threads)
             per_product = probe["seconds_per_step"] / min(1000, K)
