@@ -340,3 +340,20 @@ def test_vnd_host_width_fallback():
     bad = Instance(17, 40, -np.ones((17, 40), np.int64), small.returns, *small.arrays()[2:])
     with pytest.raises(ValueError):
         dev.vnd_host(bad, s0.setup_m, s0.setup_r)
+
+
+def test_product_stats_and_variant_guard():
+    """rl_vnd_product_stats: per-product sweeps/moves/evals of the last
+    descent add up to the totals (global sweeps = the slowest product's);
+    the removed two-products-per-warp variant bit is rejected."""
+    inst = generate_instance(GeneratorConfig(products=300, periods=52, seed=0))
+    start = initial_solution(inst)
+    dev = DeviceInstance(inst)
+    with pytest.raises(Exception):
+        dev.set_variant(1)
+    _, _, trace, st = dev.vnd(start.setup_m, start.setup_r)
+    sw, mv, ev = dev.product_stats()
+    assert int(sw.max()) == st["sweeps"] == (len(trace) - 1) // 4
+    assert int(mv.sum()) == st["moves"]
+    assert int(ev.sum()) == st["evals"]
+    assert st["cost"] == 1328299635   # live-reference golden (SURVEY.md 8(c))
