@@ -733,7 +733,10 @@ __global__ void k_list_moves(int nbh, int T, const uint8_t *sm, const uint8_t *s
 
 // ------------------------------------------------------------------ handle
 
-constexpr int kMaxChunks = 4;   // rl_vnd_host pipeline depth
+#ifndef RL_E2E_CHUNKS
+#define RL_E2E_CHUNKS 4
+#endif
+constexpr int kMaxChunks = RL_E2E_CHUNKS;   // rl_vnd_host pipeline depth (<= 12: h->ints)
 
 struct rl_instance {
     int64_t K = 0;
