@@ -38,7 +38,11 @@ typedef struct rl_instance rl_instance;
 
 /* Upload an instance once; the handle owns its device memory.
  * Replaces the Instance arrays handed to every kernel call
- * (reference model.py:28-72, vnd.py:141-145, plan.py:120-123). */
+ * (reference model.py:28-72, vnd.py:141-145, plan.py:120-123).
+ * 1 <= T <= 16000.  The move-scoring entry points keep one product's
+ * horizon in shared memory (~26 B per period with int32 values, ~38 B with
+ * int64): horizons beyond ~8,000 (int32) / ~5,800 (int64) periods return
+ * RL_EINVAL from rl_vnd / rl_scan_products / rl_product_costs. */
 int rl_instance_create(int64_t K, int64_t T, const int64_t *demand, const int64_t *returns,
                        const int64_t *setup_m, const int64_t *setup_r,
                        const int64_t *hold_m, const int64_t *hold_r,

@@ -462,15 +462,15 @@ static cudaError_t gv_alloc(GvnsState *gs, P **p, size_t bytes)
 template <typename V, typename C, typename Mask>
 static int gv_launch_vnd(rl_instance *h, GvnsState *gs)
 {
-    int grid;
+    int grid, block;
     size_t smem;
     int rc = launch_cfg<V, C>(h, (const void *)k_gvns_vnd<V, C, Mask>,
                               (int64_t)gs->a.W * gs->a.tcap + (int64_t)gs->a.fb_slots * h->K,
-                              grid, smem);
+                              grid, smem, block);
     if (rc)
         return rc;
     CK(cudaMemsetAsync(gs->a.queue, 0, sizeof(int), h->stream));
-    k_gvns_vnd<V, C, Mask><<<grid, kWarpsPerCta * 32, smem, h->stream>>>(view<V>(h), gs->a,
+    k_gvns_vnd<V, C, Mask><<<grid, block, smem, h->stream>>>(view<V>(h), gs->a,
                                                                           gs->k_vnd_max);
     CKL();
     return 0;

@@ -741,6 +741,7 @@ constexpr int kMaxChunks = RL_E2E_CHUNKS;   // rl_vnd_host pipeline depth (<= 12
 struct rl_instance {
     int64_t K = 0;
     int T = 0, vbytes = 8, cbytes = 8, device = 0, sms = 0;
+    int smem_optin = 48 * 1024;            // max dynamic shared memory per CTA (opt-in)
     cudaStream_t stream = nullptr, stream2 = nullptr, stream3 = nullptr;
     cudaEvent_t evc[kMaxChunks + 2] = {};   // rl_vnd_host: chunk copies landed, joins
     int64_t *dem64 = nullptr, *ret64 = nullptr, *cost6 = nullptr;
@@ -855,6 +856,9 @@ static int alloc_instance(rl_instance *h)
     if (e != cudaSuccess)
         return fail(RL_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
     e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
+    if (e == cudaSuccess)
+        e = cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                   h->device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking);
@@ -958,19 +962,31 @@ extern "C" void rl_instance_destroy(rl_instance *h)
 }
 
 
+// Warp-per-product kernels: kWarpsPerCta warps (one shared-memory slot each)
+// per CTA, fewer when a long horizon's slots do not fit one CTA's opt-in
+// shared memory.  Returns the block size in `block`.
 template <typename V, typename C>
-static int launch_cfg(rl_instance *h, const void *fn, int64_t nprod, int &grid, size_t &smem)
+static int launch_cfg(rl_instance *h, const void *fn, int64_t nprod, int &grid, size_t &smem,
+                      int &block)
 {
-    smem = kWarpsPerCta * slot_bytes<V, C>(h->T);
+    const size_t slot = slot_bytes<V, C>(h->T);
+    int nw = kWarpsPerCta;
+    while (nw > 1 && (size_t)nw * slot > (size_t)h->smem_optin)
+        --nw;
+    smem = nw * slot;
+    if (smem > (size_t)h->smem_optin)
+        return fail(RL_EINVAL, "T=%d needs %zu B shared memory per product (max %d)", h->T,
+                    slot, h->smem_optin);
     if (smem > 48 * 1024)
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nw * 32, smem));
     if (occ < 1)
         return fail(RL_EINVAL, "T=%d needs %zu B shared memory per CTA", h->T, smem);
-    const int64_t want = (nprod + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int64_t want = (nprod + nw - 1) / nw;
     const int64_t cap = (int64_t)h->sms * occ;
     grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+    block = nw * 32;
     return 0;
 }
 
@@ -978,6 +994,9 @@ template <typename V, typename C>
 static int launch_cfg_cta(rl_instance *h, const void *fn, int64_t nprod, int &grid, size_t &smem)
 {
     smem = slot_bytes<V, C>(h->T);
+    if (smem > (size_t)h->smem_optin)
+        return fail(RL_EINVAL, "T=%d needs %zu B shared memory per product (max %d)", h->T,
+                    smem, h->smem_optin);
     if (smem > 48 * 1024)
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -1055,11 +1074,13 @@ static int do_costs(rl_instance *h, int64_t lo, int64_t hi, int64_t *d_out)
 {
     int grid;
     size_t smem;
-    int rc = launch_cfg<V, C>(h, (const void *)k_product_costs<V, C, Mask>, hi - lo, grid, smem);
+    int block;
+    int rc = launch_cfg<V, C>(h, (const void *)k_product_costs<V, C, Mask>, hi - lo, grid, smem,
+                              block);
     if (rc)
         return rc;
     const size_t kt = (size_t)h->K * h->T;
-    k_product_costs<V, C, Mask><<<grid, kWarpsPerCta * 32, smem, h->stream>>>(
+    k_product_costs<V, C, Mask><<<grid, block, smem, h->stream>>>(
         view<V>(h), h->plan, h->plan + kt, lo, hi, d_out);
     CKL();
     return 0;
@@ -1092,12 +1113,13 @@ static int do_scan(rl_instance *h, int64_t lo, int64_t hi, int nbh)
 {
     int grid;
     size_t smem;
-    int rc = launch_cfg<V, C>(h, (const void *)k_scan<V, C, Mask>, hi - lo, grid, smem);
+    int block;
+    int rc = launch_cfg<V, C>(h, (const void *)k_scan<V, C, Mask>, hi - lo, grid, smem, block);
     if (rc)
         return rc;
     const size_t kt = (size_t)h->K * h->T;
     const int64_t K = h->K;
-    k_scan<V, C, Mask><<<grid, kWarpsPerCta * 32, smem, h->stream>>>(
+    k_scan<V, C, Mask><<<grid, block, smem, h->stream>>>(
         view<V>(h), h->plan, h->plan + kt, lo, hi, nbh, h->scan_i64, h->scan_i64 + K,
         h->scan_u8, h->scan_u8 + K, h->scan_i64 + 2 * K, h->scan_u8 + 2 * K, h->scan_u8 + 3 * K,
         h->bounds + 2);
@@ -1215,7 +1237,7 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
                             uint8_t *sm_out, uint8_t *sr_out, int64_t lo, int64_t hi, int *queue,
                             cudaStream_t st)
 {
-    int grid;
+    int grid, block = kWarpsPerCta * 32;
     size_t smem;
     const int64_t nprod = hi - lo;
     // CTA per product only when the launch is latency-bound (few products):
@@ -1231,7 +1253,7 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
                      : skip ? (const void *)k_vnd<V, C, Mask, true>
                             : (const void *)k_vnd<V, C, Mask, false>;
     int rc = cta ? launch_cfg_cta<V, C>(h, fn, nprod, grid, smem)
-                 : launch_cfg<V, C>(h, fn, nprod, grid, smem);
+                 : launch_cfg<V, C>(h, fn, nprod, grid, smem, block);
     if (rc)
         return rc;
     const VndOut o = vnd_out(h, lo, hi, queue);
@@ -1239,10 +1261,10 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
         k_vnd_cta<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
                                                                 sr_out, k_max, o);
     else if (skip)
-        k_vnd<V, C, Mask, true><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in,
+        k_vnd<V, C, Mask, true><<<grid, block, smem, st>>>(view<V>(h), sm_in, sr_in,
                                                                         sm_out, sr_out, k_max, o);
     else
-        k_vnd<V, C, Mask, false><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in,
+        k_vnd<V, C, Mask, false><<<grid, block, smem, st>>>(view<V>(h), sm_in, sr_in,
                                                                          sm_out, sr_out, k_max, o);
     CKL();
     return 0;

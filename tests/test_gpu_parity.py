@@ -357,3 +357,33 @@ def test_product_stats_and_variant_guard():
     assert int(mv.sum()) == st["moves"]
     assert int(ev.sum()) == st["evals"]
     assert st["cost"] == 1328299635   # live-reference golden
+
+
+@pytest.mark.parametrize("K,T", [(6, 3000), (2, 7000)])
+def test_long_horizon_shared_memory_limits(K, T):
+    """Horizons whose per-product shared memory does not fit four slots per
+    CTA (T=3000: ~79 KB per product) run with fewer warps per CTA; T=7000
+    (~184 KB) fits one product per CTA.  Single passes match the oracle, and
+    the descent ends in a local optimum of N1..N4 whose cost is the plan's
+    cost, identically for the CTA-per-product and warp-per-product kernels."""
+    rng = np.random.default_rng(T)
+    inst = _random_instance(rng, K, T)
+    start = initial_solution(inst)
+    dev = DeviceInstance(inst)
+    np.testing.assert_array_equal(dev.product_costs(start.setup_m, start.setup_r),
+                                  oracle.product_costs(inst, start.setup_m, start.setup_r))
+    for nbh in (1, 3):
+        out, ev = dev.scan_products(start.setup_m, start.setup_r, nbh)
+        want, oev = oracle.scan_products(inst, start.setup_m, start.setup_r, nbh)
+        assert ev == oev
+        np.testing.assert_array_equal(out[0], want[0])
+    results = []
+    for variant in (0, 2):
+        dev.set_variant(variant)
+        sm, sr, trace, st = dev.vnd(start.setup_m, start.setup_r)
+        results.append((sm.tobytes(), sr.tobytes(), trace.tolist(), st["cost"]))
+        assert st["cost"] == trace[-1] == int(dev.product_costs(sm, sr).sum())
+        for nbh in (1, 2, 3, 4):
+            out, _ = dev.scan_products(sm, sr, nbh)
+            assert not out[0].any()
+    assert results[0] == results[1]
