@@ -776,6 +776,14 @@ __device__ inline int enumerate_moves(const Slot<V, C> &s, const Mask &mk, int n
 template <typename C>
 __device__ inline void warp_argmin(C &best, int &key)
 {
+    if constexpr (sizeof(C) == 4) {
+        // two warp reductions (redux.sync): the minimum cost, then the
+        // smallest key among the lanes holding it
+        const C m = (C)__reduce_min_sync(FULL, (int)best);
+        key = (int)__reduce_min_sync(FULL, best == m ? (unsigned)key : 0xffffffffu);
+        best = m;
+        return;
+    }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
         const C ob = __shfl_xor_sync(FULL, best, off);
