@@ -772,27 +772,26 @@ __device__ inline int enumerate_moves(const Slot<V, C> &s, const Mask &mk, int n
     return n;
 }
 
-// lexicographic (cost, slot) minimum over the warp
+// lexicographic (cost, slot) minimum over the warp by redux.sync: the
+// minimum cost (int64: high words signed, then low words of the lanes
+// holding the minimal high word), then the smallest key among its lanes
 template <typename C>
 __device__ inline void warp_argmin(C &best, int &key)
 {
+    bool at;
     if constexpr (sizeof(C) == 4) {
-        // two warp reductions (redux.sync): the minimum cost, then the
-        // smallest key among the lanes holding it
         const C m = (C)__reduce_min_sync(FULL, (int)best);
-        key = (int)__reduce_min_sync(FULL, best == m ? (unsigned)key : 0xffffffffu);
+        at = best == m;
         best = m;
-        return;
+    } else {
+        const int hi = (int)((uint64_t)best >> 32);
+        const unsigned lo = (unsigned)(uint64_t)best;
+        const int mh = __reduce_min_sync(FULL, hi);
+        const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+        at = hi == mh && lo == ml;
+        best = (C)(((uint64_t)(uint32_t)mh << 32) | ml);
     }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-        const C ob = __shfl_xor_sync(FULL, best, off);
-        const int ok = __shfl_xor_sync(FULL, key, off);
-        if (ob < best || (ob == best && ok < key)) {
-            best = ob;
-            key = ok;
-        }
-    }
+    key = (int)__reduce_min_sync(FULL, at ? (unsigned)key : 0xffffffffu);
 }
 
 // Score the moves i = wi, wi + nw, wi + 2 nw, ... (< n) of the current list
