@@ -752,6 +752,69 @@ __device__ inline typename PatchOf<Mask>::type patch_of(const Mask &mk, const Mo
 // increasing slot order, so a strict '<' keeps the earliest on ties.
 // Move list of neighborhood nbh for the warp's product: N1/N2 are dense
 // (slot = index, returns T), N3/N4 are compacted into s.mv.
+// Register rows (T <= 63): the N3/N4 validity masks are bit operations on
+// the rows (N3 row x: left shifts x & ~(x << 1) minus period 0, right shifts
+// x & ~(x >> 1) below T - 1; N4: M ^ R), so each lane places its periods t
+// and t + 32 with prefix popcounts in one round (slot order = row*2T + 2t +
+// dir, the reference's list_moves order).
+struct RegMoveMasks {
+    uint64_t lm, rm, lr, rr;   // N3 left/right shifts of the M and R rows
+};
+__device__ inline RegMoveMasks reg_move_masks(const MaskReg &mk)
+{
+    const int T = mk.T;
+    const uint64_t all = (1ull << T) - 1, nolast = (1ull << (T - 1)) - 1;
+    RegMoveMasks r;
+    r.lm = mk.M & ~(mk.M << 1) & all & ~1ull;
+    r.rm = mk.M & ~(mk.M >> 1) & nolast;
+    r.lr = mk.R & ~(mk.R << 1) & all & ~1ull;
+    r.rr = mk.R & ~(mk.R >> 1) & nolast;
+    return r;
+}
+
+template <typename V, typename C>
+__device__ inline int enumerate_moves(const Slot<V, C> &s, const MaskReg &mk, int nbh, int T,
+                                      int lane)
+{
+    if (nbh <= 2)
+        return T;
+    int n;
+    if (nbh == 4) {
+        const uint64_t x = (mk.M ^ mk.R) & ((1ull << T) - 1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = lane + 32 * h;
+            if (t < T && ((x >> t) & 1))
+                s.mv[__popcll(x & ((1ull << t) - 1))] = (uint16_t)t;
+        }
+        n = __popcll(x);
+    } else {
+        const RegMoveMasks q = reg_move_masks(mk);
+        const int nm = __popcll(q.lm) + __popcll(q.rm);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = lane + 32 * h;
+            if (t < T) {
+                const uint64_t below = (1ull << t) - 1;
+                const int pm = __popcll(q.lm & below) + __popcll(q.rm & below);
+                const int pr = nm + __popcll(q.lr & below) + __popcll(q.rr & below);
+                const int lm = (q.lm >> t) & 1, lr = (q.lr >> t) & 1;
+                if (lm)
+                    s.mv[pm] = (uint16_t)(2 * t);
+                if ((q.rm >> t) & 1)
+                    s.mv[pm + lm] = (uint16_t)(2 * t + 1);
+                if (lr)
+                    s.mv[pr] = (uint16_t)(2 * T + 2 * t);
+                if ((q.rr >> t) & 1)
+                    s.mv[pr + lr] = (uint16_t)(2 * T + 2 * t + 1);
+            }
+        }
+        n = nm + __popcll(q.lr) + __popcll(q.rr);
+    }
+    __syncwarp();
+    return n;
+}
+
 template <typename V, typename C, typename Mask>
 __device__ inline int enumerate_moves(const Slot<V, C> &s, const Mask &mk, int nbh, int T,
                                       int lane)
@@ -996,6 +1059,16 @@ __device__ inline void apply_slot(Mask &mk, int nbh, int slot, int T, int lane)
 
 // Move count of one neighborhood at the current plan (used to credit the
 // lockstep passes a product sits out after reaching its fixpoint).
+__device__ inline int move_count(const MaskReg &mk, int nbh, int T, int)
+{
+    if (nbh <= 2)
+        return T;
+    if (nbh == 4)
+        return __popcll((mk.M ^ mk.R) & ((1ull << T) - 1));
+    const RegMoveMasks q = reg_move_masks(mk);
+    return __popcll(q.lm) + __popcll(q.rm) + __popcll(q.lr) + __popcll(q.rr);
+}
+
 template <typename Mask>
 __device__ inline int move_count(const Mask &mk, int nbh, int T, int lane)
 {
