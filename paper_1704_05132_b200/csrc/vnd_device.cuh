@@ -139,6 +139,9 @@ struct Slot {
     uint64_t *bar;
 };
 
+#ifndef RL_REFILL_MIN
+#define RL_REFILL_MIN 16   // measured: 1 -> 20.1, 8 -> 19.1, 16 -> 18.8, 24 -> 18.9 ms at C3
+#endif
 constexpr int kSlackLevels = 16;   // lm[j] = slack < 2^j (j < 16), lm[16] = all sR, lm[17] = slack < 0
 // The slack-level skip (scan_pass) shortens long delta walks, which pays
 // when the descent is latency-bound (few products per SM, GVNS tasks) and
@@ -995,11 +998,15 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
         }
         const unsigned m = __ballot_sync(FULL, state == 0);
         const bool more = m != FULL || next * nw + wi < n;
-        if (state == 0) {
-            gi = (next + __popc(m & lt)) * nw + wi;
-            state = gi < n ? 1 : 0;
+        // refill idle lanes in batches (the set-up branch costs the whole
+        // warp's issue slots however few lanes take a move)
+        if (m == FULL || __popc(m) >= RL_REFILL_MIN) {
+            if (state == 0) {
+                gi = (next + __popc(m & lt)) * nw + wi;
+                state = gi < n ? 1 : 0;
+            }
+            next += __popc(m);
         }
-        next += __popc(m);
         if (!more)
             break;
     }
