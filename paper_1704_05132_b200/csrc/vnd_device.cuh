@@ -139,6 +139,9 @@ struct Slot {
     uint64_t *bar;
 };
 
+#ifndef RL_WORD_ENUM_MIN_T
+#define RL_WORD_ENUM_MIN_T 128
+#endif
 #ifndef RL_REFILL_MIN
 #define RL_REFILL_MIN 16   // measured: 1 -> 20.1, 8 -> 19.1, 16 -> 18.8, 24 -> 18.9 ms at C3
 #endif
@@ -818,9 +821,118 @@ __device__ inline int enumerate_moves(const Slot<V, C> &s, const MaskReg &mk, in
     return n;
 }
 
-template <typename V, typename C, typename Mask>
-__device__ inline int enumerate_moves(const Slot<V, C> &s, const Mask &mk, int nbh, int T,
+// Shared-memory rows (T > 63): the same masks word by word (lane w owns
+// periods 32w..32w+31, T <= 32 x 32 here is not assumed: lanes loop over
+// words), warp prefix sums of the per-word counts, and each lane writes its
+// word's slots in period order.
+struct WordMoveMasks {
+    uint32_t lm, rm, lr, rr, sw;   // N3 left/right of the M and R rows, N4
+};
+__device__ inline WordMoveMasks word_move_masks(const MaskSmem &mk, int w, int NW)
+{
+    const int T = mk.T;
+    const uint32_t m = mk.bm[w], r = mk.br[w];
+    const uint32_t mp = w > 0 ? mk.bm[w - 1] : 0u, rp = w > 0 ? mk.br[w - 1] : 0u;
+    const uint32_t mn = w + 1 < NW ? mk.bm[w + 1] : 0u, rn = w + 1 < NW ? mk.br[w + 1] : 0u;
+    const int base = 32 * w;
+    const uint32_t in_t = T - base >= 32 ? 0xffffffffu : (1u << (T - base)) - 1;      // t < T
+    const uint32_t in_t1 = T - 1 - base >= 32 ? 0xffffffffu
+                           : T - 1 - base <= 0 ? 0u : (1u << (T - 1 - base)) - 1;   // t + 1 < T
+    const uint32_t not0 = w == 0 ? ~1u : 0xffffffffu;                                // t > 0
+    WordMoveMasks q;
+    q.lm = m & ~((m << 1) | (mp >> 31)) & in_t & not0;
+    q.rm = m & ~((m >> 1) | (mn << 31)) & in_t1;
+    q.lr = r & ~((r << 1) | (rp >> 31)) & in_t & not0;
+    q.rr = r & ~((r >> 1) | (rn << 31)) & in_t1;
+    q.sw = (m ^ r) & in_t;
+    return q;
+}
+
+template <typename C>
+__device__ inline int warp_excl_scan(int x, int lane, int &total)
+{
+    int incl = x;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(FULL, incl, off);
+        if (lane >= off)
+            incl += o;
+    }
+    total = __shfl_sync(FULL, incl, 31);
+    return incl - x;
+}
+
+template <typename V, typename C>
+__device__ inline int enumerate_moves(const Slot<V, C> &s, const MaskSmem &mk, int nbh, int T,
                                       int lane)
+{
+    if (nbh <= 2)
+        return T;
+    // few words: ballot rounds (the two are within noise up to T ~ 130;
+    // the word path wins at C4: 214 -> 196 ms)
+    if (T <= RL_WORD_ENUM_MIN_T)
+        return enumerate_moves_ballot(s, mk, nbh, T, lane);
+    const int NW = (T + 31) >> 5;
+    int n = 0;   // slots written by earlier word groups
+    for (int w0 = 0; w0 < NW; w0 += 32) {
+        const int w = w0 + lane;
+        WordMoveMasks q{0u, 0u, 0u, 0u, 0u};
+        if (w < NW)
+            q = word_move_masks(mk, w, NW);
+        if (nbh == 4) {
+            int tot;
+            int pos = n + warp_excl_scan<C>(__popc(q.sw), lane, tot);
+            for (uint32_t x = q.sw; x; x &= x - 1)
+                s.mv[pos++] = (uint16_t)(32 * w + __ffs(x) - 1);
+            n += tot;
+        } else {
+            // row M slots of every word come before row R slots of any word,
+            // so the M counts are scanned over all word groups first
+            int totm;
+            int pm = warp_excl_scan<C>(__popc(q.lm) + __popc(q.rm), lane, totm);
+            (void)pm;
+            n += totm;
+        }
+    }
+    if (nbh == 4) {
+        __syncwarp();
+        return n;
+    }
+    // N3: second sweep writes the slots (row M at [0, nM), row R after)
+    const int nM = n;
+    int om = 0, orr = nM;
+    for (int w0 = 0; w0 < NW; w0 += 32) {
+        const int w = w0 + lane;
+        WordMoveMasks q{0u, 0u, 0u, 0u, 0u};
+        if (w < NW)
+            q = word_move_masks(mk, w, NW);
+        int tm, tr;
+        int pm = om + warp_excl_scan<C>(__popc(q.lm) + __popc(q.rm), lane, tm);
+        int pr = orr + warp_excl_scan<C>(__popc(q.lr) + __popc(q.rr), lane, tr);
+        for (uint32_t x = q.lm | q.rm; x; x &= x - 1) {
+            const int i = __ffs(x) - 1, t = 32 * w + i;
+            if ((q.lm >> i) & 1)
+                s.mv[pm++] = (uint16_t)(2 * t);
+            if ((q.rm >> i) & 1)
+                s.mv[pm++] = (uint16_t)(2 * t + 1);
+        }
+        for (uint32_t x = q.lr | q.rr; x; x &= x - 1) {
+            const int i = __ffs(x) - 1, t = 32 * w + i;
+            if ((q.lr >> i) & 1)
+                s.mv[pr++] = (uint16_t)(2 * T + 2 * t);
+            if ((q.rr >> i) & 1)
+                s.mv[pr++] = (uint16_t)(2 * T + 2 * t + 1);
+        }
+        om += tm;
+        orr += tr;
+    }
+    __syncwarp();
+    return orr;
+}
+
+template <typename V, typename C, typename Mask>
+__device__ inline int enumerate_moves_ballot(const Slot<V, C> &s, const Mask &mk, int nbh, int T,
+                                             int lane)
 {
     if (nbh <= 2)
         return T;
@@ -1074,6 +1186,19 @@ __device__ inline int move_count(const MaskReg &mk, int nbh, int T, int)
         return __popcll((mk.M ^ mk.R) & ((1ull << T) - 1));
     const RegMoveMasks q = reg_move_masks(mk);
     return __popcll(q.lm) + __popcll(q.rm) + __popcll(q.lr) + __popcll(q.rr);
+}
+
+__device__ inline int move_count(const MaskSmem &mk, int nbh, int T, int lane)
+{
+    if (nbh <= 2)
+        return T;
+    const int NW = (T + 31) >> 5;
+    int c = 0;
+    for (int w = lane; w < NW; w += 32) {
+        const WordMoveMasks q = word_move_masks(mk, w, NW);
+        c += nbh == 4 ? __popc(q.sw) : __popc(q.lm) + __popc(q.rm) + __popc(q.lr) + __popc(q.rr);
+    }
+    return __reduce_add_sync(FULL, (unsigned)c);
 }
 
 template <typename Mask>

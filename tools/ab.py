@@ -12,7 +12,7 @@ from paper_1704_05132_b200 import GeneratorConfig, generate_instance  # noqa: E4
 from paper_1704_05132_b200._native import DeviceInstance  # noqa: E402
 
 SIZES = {"c3": (100000, 52), "c2": (1000, 52), "c4": (10000, 520), "c4s": (100, 520),
-         "t30": (20000, 30), "t63": (20000, 63), "t64": (20000, 64), "t100": (20000, 100), "t200": (10000, 200), "k100": (100, 52), "k500": (500, 52)}
+         "t30": (20000, 30), "t63": (20000, 63), "t64": (20000, 64), "t100": (20000, 100), "t200": (10000, 200), "t130": (15000, 130), "k100": (100, 52), "k500": (500, 52)}
 names = sys.argv[1].split(",")
 variants = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
