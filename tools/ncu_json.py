@@ -46,6 +46,9 @@ summary = {
     "warp_inst": int(num("smsp__inst_executed.sum")),
     "registers": int(num("launch__registers_per_thread")),
     "smem_wavefronts": int(num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")),
+    "smem_pipe_pct": round(
+        num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"), 1),
+    "dram_gbs": round((rd + wr) / (num("gpu__time_duration.sum") * 1e-3) / 1e9, 2),
 }
 for name, obj in (("traffic", traffic), ("ncu", summary)):
     path = os.path.join(ROOT, "profiles", f"k_vnd_{wl}_{name}.json")
