@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build compile-time variants of the library and time them (dev experiment).
-#   tools/variants.sh "-DRL_NO_SKIP" "-DRL_VND_MINB=5" ...
+#   AB_CONFIGS=c3,c4 tools/variants.sh "-DRL_REFILL_MIN=8" "-DRL_VND_MINB=5" ...
 set -e
 i=0
 for flags in "$@"; do
@@ -13,6 +13,6 @@ wait
 i=0
 for flags in "$@"; do
   echo "== variant $i: $flags"
-  REMLOT_B200_LIB=$PWD/paper_1704_05132_b200/_lib/libremlot_b200_v$i.so python tools/quick_time.py | grep "packed=0\|T=520"
+  REMLOT_B200_LIB=$PWD/paper_1704_05132_b200/_lib/libremlot_b200_v$i.so python tools/ab.py ${AB_CONFIGS:-c2,c3,c4} 0 3
   i=$((i+1))
 done
