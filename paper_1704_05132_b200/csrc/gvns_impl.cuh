@@ -90,6 +90,18 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
 {
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (blockIdx.x == 0) {
+        // per-round counters of the kernels after this one (fallback slots,
+        // fallback plan costs, the VND task queue): reset here instead of by
+        // three memset nodes per round
+        if (threadIdx.x == 0) {
+            g.scal[GV_FB_COUNT] = 0;
+            g.scal[GV_FB_COUNT + 1] = 0;
+            *g.queue = 0;
+        }
+        for (int i = threadIdx.x; i < g.fb_slots; i += blockDim.x)
+            g.scal[GV_FBCOST0 + i] = 0;
+    }
     if (w >= g.W)
         return;
     Philox rng;
@@ -469,7 +481,6 @@ static int gv_launch_vnd(rl_instance *h, GvnsState *gs)
                               grid, smem, block);
     if (rc)
         return rc;
-    CK(cudaMemsetAsync(gs->a.queue, 0, sizeof(int), h->stream));
     k_gvns_vnd<V, C, Mask><<<grid, block, smem, h->stream>>>(view<V>(h), gs->a,
                                                                           gs->k_vnd_max);
     CKL();
@@ -480,8 +491,6 @@ template <typename V, typename C>
 static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round)
 {
     const int W = gs->a.W;
-    CK(cudaMemsetAsync(&gs->a.scal[GV_FB_COUNT], 0, 2 * sizeof(int64_t), h->stream));
-    CK(cudaMemsetAsync(&gs->a.scal[GV_FBCOST0], 0, gs->a.fb_slots * sizeof(int64_t), h->stream));
     k_shake<V><<<(W + 3) / 4, 128, 0, h->stream>>>(view<V>(h), gs->a, round);
     CKL();
     k_shake_fallback<V><<<(W + 63) / 64, 64, 0, h->stream>>>(view<V>(h), gs->a);
