@@ -159,7 +159,7 @@ __host__ __device__ inline size_t slot_bytes(int T)
     const int NW = (T + 31) >> 5;
     size_t b = 0;
     b += align16((size_t)(T + 1) * sizeof(DR<V>));      // dr
-    b += align16(XCStore<V, C>::bytes(T));             // xc
+    b += align16(XCStore<V, C>::bytes(T + 1));         // xc (+ the end entry xc[T])
     b += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));   // slk (register-mask path only)
     b += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));   // nx
     b += align16(2 * (size_t)NW * sizeof(uint32_t));
@@ -176,7 +176,7 @@ __device__ inline Slot<V, C> carve(unsigned char *base, int T)
     Slot<V, C> s;
     unsigned char *p = base;
     s.dr = (DR<V> *)p; p += align16((size_t)(T + 1) * sizeof(DR<V>));
-    s.xc.carve(p, T); p += align16(XCStore<V, C>::bytes(T));
+    s.xc.carve(p, T + 1); p += align16(XCStore<V, C>::bytes(T + 1));
     // the staged demand/returns rows (2T x V <= the xc area) are consumed by
     // build_prefix before base_pass first writes xc
     s.stage = (V *)s.xc.base();
@@ -638,6 +638,8 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
             if (mk.m(u) | mk.r(u))
                 s.xc.add_c(u, excl);
     S = __shfl_sync(FULL, incl, 31);
+    if (lane == 0)
+        s.xc.set(T, V(0), S);   // end entry: a walk reaching T adds S - S
     const int f = mk.next(0);
     ok = ok && s.dr[f].d == 0;   // demand before the first setup (_kernels.py:58-60)
     const bool feas = __all_sync(FULL, ok);
@@ -1065,7 +1067,7 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
             C c;
             V xr;
             const bool ok = seg_cost<V, C>(cdu, cru, ev.d, u, mu, ru, X, pc, c, xr);
-            const XC<V, C> bv = s.xc[v < T ? v : T - 1];
+            const XC<V, C> bv = s.xc[v];   // v <= T; xc[T].c = S
             acc += c;
             X += xr;
             // past the move the rows equal the base plan's; only X may differ
@@ -1086,7 +1088,7 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
                 sync = past && (delta == 0 || q >= T);
                 total = acc + (S - bv.c);
                 const int qq = past && q < T ? q : v;
-                const XC<V, C> bq = s.xc[qq < T ? qq : T - 1];
+                const XC<V, C> bq = s.xc[qq];
                 const DR<V> eq = s.dr[qq];
                 acc += bq.c - bv.c;   // 0 unless past (qq == v otherwise)
                 X = past ? bq.x + delta : X;
@@ -1101,8 +1103,9 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
                 cdu = ev.d;
                 cru = ev.r;
             }
+            // total = acc + S - cpre[v]: the base suffix when resynced, and
+            // just acc at v = T (xc[T].c = S); only read when fin
             const bool fin = v >= T || sync;
-            total = sync ? total : acc;
             const bool take = ok && fin && total < best;
             best = take ? total : best;
             key = take ? slot : key;
