@@ -999,11 +999,12 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
     int state = gi < n ? 1 : 0;
     int next = 32;   // move indices handed out so far (in units of this warp's share)
 #ifdef RL_WALK_STATS
-    int ws_cur = 0, ws_max = 0, ws_lane = 0, ws_it = 0;
+    int ws_cur = 0, ws_max = 0, ws_lane = 0, ws_it = 0, ws_pend = 0;
 #endif
     for (;;) {
 #ifdef RL_WALK_STATS
         ++ws_it;
+        ws_pend += __any_sync(FULL, state == 1);
         if (state == 1 && ws_cur) {
             atomicAdd(&g_walk_stats[8 + min(ws_cur, 63)], 1ull);
             ws_max = max(ws_max, ws_cur);
@@ -1145,6 +1146,7 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
         atomicAdd(&g_walk_stats[4], (unsigned long long)mx);
         atomicAdd(&g_walk_stats[5], (unsigned long long)busy);
         atomicAdd(&g_walk_stats[72 + min(ws_it, 63)], 1ull);
+        atomicAdd(&g_walk_stats[6], (unsigned long long)ws_pend);
     }
 #endif
 }

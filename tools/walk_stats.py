@@ -35,7 +35,8 @@ for name, variant in [(n, v) for n in (sys.argv[1:] or ["c2", "c3"]) for v in va
     P, it, n, steps, mx, busy = (int(x) for x in buf[:6])
     print(f"{name} K={K} T={T} variant {variant}: passes {P}, moves/pass {n / P:.1f}, steps/move {steps / n:.2f}, "
           f"iterations/pass {it / P:.2f}, longest walk/pass {mx / P:.2f}, busiest lane/pass "
-          f"{busy / P:.2f}, lane utilisation {steps / (32 * it):.3f}")
+          f"{busy / P:.2f}, lane utilisation {steps / (32 * it):.3f}, set-up branches/pass "
+          f"{int(buf[6]) / P:.2f}")
     h = buf[8:72]
     print("  walk-length histogram (len:count%): " +
           " ".join(f"{i}:{100 * h[i] / h.sum():.1f}" for i in range(64) if h[i] * 1000 > h.sum()))
