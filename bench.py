@@ -361,10 +361,15 @@ def main():
             per_product = probe["seconds_per_step"] / min(1000, K)
             sample = int(min(K, max(1000, 12.0 / max(per_product, 1e-9))))
             r = cpu_reference(inst, sample, 1, 0, threads)
+            # and one core (serial and product-parallel)
+            s1 = max(100, min(K, int(sample * 3.0 / max(r["seconds_per_step"] * threads, 1e-9))))
+            r1 = cpu_reference(inst, s1, 1, 0, 1)
             line["cpu_baseline"] = {
                 "value": r["value"], "unit": "evals/s", "cores": threads, "kind": "port",
                 "sample": f"first {sample} products, lockstep VND to local optimum "
-                          f"({r['seconds_per_step']:.2f} s)"}
+                          f"({r['seconds_per_step']:.2f} s)",
+                "serial": {"value": r1["value"], "cores": 1,
+                           "sample": f"first {s1} products ({r1['seconds_per_step']:.2f} s)"}}
         if world == 1 and not args.no_extra:
             line["other_configs"] = devbench.other_configs(torch)
         if args.workload == "c3" and K == 100_000:
