@@ -372,6 +372,16 @@ def main():
                            "sample": f"first {s1} products ({r1['seconds_per_step']:.2f} s)"}}
         if world == 1 and not args.no_extra:
             line["other_configs"] = devbench.other_configs(torch)
+            if not args.no_cpu_baseline:
+                # C4's CPU reference rate on a bounded sample (the full run
+                # is ~80 min on 8 threads)
+                inst4 = generate_instance(GeneratorConfig(products=10000, periods=520, seed=0))
+                n4 = 4 * threads
+                r4 = cpu_reference(inst4, n4, 1, 0, threads)
+                line["other_configs"]["c4_vnd"]["cpu_baseline"] = {
+                    "value": r4["value"], "unit": "evals/s", "cores": threads, "kind": "port",
+                    "sample": f"first {n4} products, VND to local optimum "
+                              f"({r4['seconds_per_step']:.2f} s)"}
         if args.workload == "c3" and K == 100_000:
             line["parity"] = {"final_cost": final_cost, "reference_final_cost": 449100704810,
                               "bit_exact": final_cost == 449100704810,
