@@ -18,6 +18,7 @@ struct GvnsArgs {
     int64_t K, KT, pop;
     int64_t w0;                       // global index of local worker 0 (sharded rounds)
     int T, NW, W, k_max, kcap, tcap, tsize, fb_slots;
+    int shake_bytes;                  // per-worker shared scratch of k_shake (0: global)
     uint64_t seed;
     uint8_t *inc, *F, *init, *cand;   // 2KT bytes each: m rows then r rows
     int64_t *Fcost;                   // K
@@ -88,6 +89,7 @@ __device__ inline bool row_feasible(const V *d, const V *r, int T, BitM bm, BitR
 template <typename V>
 __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
 {
+    extern __shared__ __align__(16) unsigned char shk[];
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (blockIdx.x == 0) {
@@ -109,17 +111,32 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
         rng.seed(g.seed, (uint64_t)round, (uint64_t)(g.w0 + w));
     const int64_t strength = g.scal[GV_STRENGTH];
     const int64_t k_eff = strength < g.pop ? strength : g.pop;   // gvns.py:113
+    const int T = g.T, NW = g.NW;
+    // the draw's scratch (Floyd table, positions, touched rows) lives in
+    // shared memory when it fits: the sequential draw and feasibility walk
+    // then wait on shared-memory instead of L2 latencies; the accepted
+    // touched rows are copied out for k_gvns_vnd
     int64_t *P = g.pos + (int64_t)w * g.kcap;
     int64_t *tp = g.tp + (int64_t)w * g.tcap;
-    uint32_t *tw = g.tw + (int64_t)w * g.tcap * 2 * g.NW;
-    const int T = g.T, NW = g.NW;
+    uint32_t *tw = g.tw + (int64_t)w * g.tcap * 2 * NW;
+    uint64_t *table = g.table + (int64_t)w * g.tsize;
+    if (g.shake_bytes) {
+        unsigned char *b = shk + (size_t)(threadIdx.x >> 5) * g.shake_bytes;
+        table = (uint64_t *)b;
+        b += align16((size_t)g.tsize * 8);
+        P = (int64_t *)b;
+        b += align16((size_t)g.kcap * 8);
+        tp = (int64_t *)b;
+        b += align16((size_t)g.tcap * 8);
+        tw = (uint32_t *)b;
+    }
     for (int attempt = 0; attempt < 50; ++attempt) {   // _SHAKE_REDRAWS (gvns.py:29, :114)
         int n = 0;
         if (lane == 0) {
             if (choice_uses_tail_shuffle(g.pop, k_eff))
                 choice_tail(rng, g.pop, k_eff, P, g.tailidx + (int64_t)w * g.pop);
             else
-                choice_floyd(rng, g.pop, k_eff, P, g.table + (int64_t)w * g.tsize);
+                choice_floyd(rng, g.pop, k_eff, P, table);
             for (int64_t i = 0; i < k_eff; ++i) {   // distinct touched products
                 RL_ASSERT(P[i] >= 0 && P[i] < g.pop);
                 const int64_t k = (P[i] % g.KT) / T;
@@ -174,6 +191,14 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
         }
         ok = __shfl_sync(FULL, (int)ok, 0);
         if (ok) {
+            if (g.shake_bytes) {
+                __syncwarp();   // lane 0 wrote the scratch
+                for (int j = lane; j < n; j += 32)
+                    g.tp[(int64_t)w * g.tcap + j] = tp[j];
+                uint32_t *gw = g.tw + (int64_t)w * g.tcap * 2 * NW;
+                for (int i = lane; i < n * 2 * NW; i += 32)
+                    gw[i] = tw[i];
+            }
             if (lane == 0) {
                 g.tn[w] = n;
                 g.fb[w] = 0;
@@ -491,7 +516,8 @@ template <typename V, typename C>
 static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round)
 {
     const int W = gs->a.W;
-    k_shake<V><<<(W + 3) / 4, 128, 0, h->stream>>>(view<V>(h), gs->a, round);
+    k_shake<V><<<(W + 3) / 4, 128, 4 * (size_t)gs->a.shake_bytes, h->stream>>>(view<V>(h), gs->a,
+                                                                            round);
     CKL();
     k_shake_fallback<V><<<(W + 63) / 64, 64, 0, h->stream>>>(view<V>(h), gs->a);
     CKL();
@@ -527,6 +553,11 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset,
         a.kcap = (int)keff_max;
         a.tcap = (int)(keff_max < K ? keff_max : K);
         a.tsize = (int)(choice_table_mask(keff_max) + 1);
+        {
+            const size_t b = align16((size_t)a.tsize * 8) + align16((size_t)a.kcap * 8) +
+                             align16((size_t)a.tcap * 8) + align16((size_t)a.tcap * 2 * NW * 4);
+            a.shake_bytes = 4 * b <= 48 * 1024 ? (int)b : 0;
+        }
         const double per_slot = (double)pop * (1 + 8) + 8.0 * K;
         int fbs = (int)(512.0 * (1 << 20) / per_slot);
         fbs = fbs < 1 ? 1 : fbs;
