@@ -120,6 +120,7 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
     int64_t *tp = g.tp + (int64_t)w * g.tcap;
     uint32_t *tw = g.tw + (int64_t)w * g.tcap * 2 * NW;
     uint64_t *table = g.table + (int64_t)w * g.tsize;
+    V *drow = nullptr;
     if (g.shake_bytes) {
         unsigned char *b = shk + (size_t)(threadIdx.x >> 5) * g.shake_bytes;
         table = (uint64_t *)b;
@@ -129,6 +130,8 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
         tp = (int64_t *)b;
         b += align16((size_t)g.tcap * 8);
         tw = (uint32_t *)b;
+        b += align16((size_t)g.tcap * 2 * NW * 4);
+        drow = (V *)b;   // the touched products' demand / returns rows
     }
     for (int attempt = 0; attempt < 50; ++attempt) {   // _SHAKE_REDRAWS (gvns.py:29, :114)
         int n = 0;
@@ -163,9 +166,16 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
                     row[NW + (base >> 5)] = wr;
                 }
             }
-            for (int t = lane; t < T; t += 32) {   // warm L1 for lane 0's walk
-                (void)__ldg(in.dem + k * T + t);
-                (void)__ldg(in.ret + k * T + t);
+            if (drow) {   // stage the rows for lane 0's walk
+                for (int t = lane; t < T; t += 32) {
+                    drow[(int64_t)j * 2 * T + t] = in.dem[k * T + t];
+                    drow[(int64_t)j * 2 * T + T + t] = in.ret[k * T + t];
+                }
+            } else {
+                for (int t = lane; t < T; t += 32) {   // warm L1 for lane 0's walk
+                    (void)__ldg(in.dem + k * T + t);
+                    (void)__ldg(in.ret + k * T + t);
+                }
             }
         }
         __syncwarp();
@@ -184,7 +194,9 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
             for (int j = 0; j < n && ok; ++j) {
                 const uint32_t *row = tw + (int64_t)j * 2 * NW;
                 const int64_t k = tp[j];
-                ok = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
+                const V *dd = drow ? drow + (int64_t)j * 2 * T : in.dem + k * T;
+                const V *rr = drow ? drow + (int64_t)j * 2 * T + T : in.ret + k * T;
+                ok = row_feasible<V>(dd, rr, T,
                                      [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
                                      [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
             }
@@ -555,7 +567,8 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset,
         a.tsize = (int)(choice_table_mask(keff_max) + 1);
         {
             const size_t b = align16((size_t)a.tsize * 8) + align16((size_t)a.kcap * 8) +
-                             align16((size_t)a.tcap * 8) + align16((size_t)a.tcap * 2 * NW * 4);
+                             align16((size_t)a.tcap * 8) + align16((size_t)a.tcap * 2 * NW * 4) +
+                             align16((size_t)a.tcap * 2 * T * h->vbytes);
             a.shake_bytes = 4 * b <= 48 * 1024 ? (int)b : 0;
         }
         const double per_slot = (double)pop * (1 + 8) + 8.0 * K;
