@@ -50,6 +50,40 @@ enum {
     GV_FBCOST0,   // fb_slots entries follow
 };
 
+// The same test segment by segment over prefix sums cd[t] = sum_{i<t} D,
+// cr[t] = sum_{i<t} R (closed form of DESIGN.md 3: x_R = min(seg, cr[u+1] -
+// X) at sR setups): one iteration per setup instead of per period.
+template <typename V>
+__device__ inline bool row_feasible_prefix(const V *cd, const V *cr, int T, const uint32_t *row,
+                                           int NW)
+{
+    auto next_setup = [&](int x) {   // first setup >= x, T if none
+        if (x >= T)
+            return T;
+        int w = x >> 5;
+        uint32_t bits = (row[w] | row[NW + w]) & (0xffffffffu << (x & 31));
+        while (!bits && ++w < NW)
+            bits = row[w] | row[NW + w];
+        return bits ? min((w << 5) + __ffs(bits) - 1, T) : T;
+    };
+    int u = next_setup(0);
+    if (cd[u] > 0)
+        return false;   // demand before the first setup (_kernels.py:58-60)
+    V X = 0;
+    while (u < T) {
+        const int v = next_setup(u + 1);
+        const V seg = cd[v] - cd[u];
+        const bool m = (row[u >> 5] >> (u & 31)) & 1u, r = (row[NW + (u >> 5)] >> (u & 31)) & 1u;
+        const V avail = cr[u + 1] - X;
+        const V xr = r ? (seg < avail ? seg : avail) : V(0);
+        if (seg - xr > 0 && !m)
+            return false;
+        X += xr;
+        u = v;
+    }
+    return true;
+}
+
 // Feasibility of one product's rows under row_cost (_kernels.py:58-82):
 // no demand before the first setup, and every segment whose demand exceeds
 // the remanufactured quantity has a manufacturing setup.
@@ -166,10 +200,33 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
                     row[NW + (base >> 5)] = wr;
                 }
             }
-            if (drow) {   // stage the rows for lane 0's walk
-                for (int t = lane; t < T; t += 32) {
-                    drow[(int64_t)j * 2 * T + t] = in.dem[k * T + t];
-                    drow[(int64_t)j * 2 * T + T + t] = in.ret[k * T + t];
+            if (drow) {   // prefix sums of the rows for lane 0's segment walk
+                V *cd = drow + (int64_t)j * 2 * (T + 1), *cr = cd + T + 1;
+                V cdc = 0, crc = 0;
+                if (lane == 0) {
+                    cd[0] = 0;
+                    cr[0] = 0;
+                }
+                for (int base = 0; base < T; base += 32) {
+                    const int t = base + lane;
+                    V d = t < T ? in.dem[k * T + t] : V(0);
+                    V r = t < T ? in.ret[k * T + t] : V(0);
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const V od = __shfl_up_sync(FULL, d, off), orr = __shfl_up_sync(FULL, r, off);
+                        if (lane >= off) {
+                            d += od;
+                            r += orr;
+                        }
+                    }
+                    d += cdc;
+                    r += crc;
+                    if (t < T) {
+                        cd[t + 1] = d;
+                        cr[t + 1] = r;
+                    }
+                    cdc = __shfl_sync(FULL, d, 31);
+                    crc = __shfl_sync(FULL, r, 31);
                 }
             } else {
                 for (int t = lane; t < T; t += 32) {   // warm L1 for lane 0's walk
@@ -194,8 +251,12 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
             for (int j = 0; j < n && ok; ++j) {
                 const uint32_t *row = tw + (int64_t)j * 2 * NW;
                 const int64_t k = tp[j];
-                const V *dd = drow ? drow + (int64_t)j * 2 * T : in.dem + k * T;
-                const V *rr = drow ? drow + (int64_t)j * 2 * T + T : in.ret + k * T;
+                if (drow) {
+                    const V *cd = drow + (int64_t)j * 2 * (T + 1);
+                    ok = row_feasible_prefix<V>(cd, cd + T + 1, T, row, NW);
+                    continue;
+                }
+                const V *dd = in.dem + k * T, *rr = in.ret + k * T;
                 ok = row_feasible<V>(dd, rr, T,
                                      [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
                                      [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
@@ -568,7 +629,7 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset,
         {
             const size_t b = align16((size_t)a.tsize * 8) + align16((size_t)a.kcap * 8) +
                              align16((size_t)a.tcap * 8) + align16((size_t)a.tcap * 2 * NW * 4) +
-                             align16((size_t)a.tcap * 2 * T * h->vbytes);
+                             align16((size_t)a.tcap * 2 * (T + 1) * h->vbytes);
             a.shake_bytes = 4 * b <= 48 * 1024 ? (int)b : 0;
         }
         const double per_slot = (double)pop * (1 + 8) + 8.0 * K;
