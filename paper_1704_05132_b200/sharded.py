@@ -143,7 +143,9 @@ def sharded_gvns(inst, config, group=None, backend=None, start_plan=None):
     worker) and takes the minimum (lowest worker on ties, gvns.py:170-174),
     the winning rank broadcasts its candidate plan, and every rank applies
     the acceptance and strength step (gvns.py:207-215) identically.  The
-    wall-clock budget is decided on rank 0 and broadcast each round.
+    wall-clock budget is decided on rank 0 and travels in the same
+    all-gather (one collective per round, plus the plan broadcast when the
+    incumbent improves).
     Returns the reference's GvnsResult on every rank."""
     import time
 
@@ -172,22 +174,27 @@ def sharded_gvns(inst, config, group=None, backend=None, start_plan=None):
     inc_cost = be.begin(max(local, 1), w_lo, config, sm0, sr0)
     strength, rounds = 1, 0
     BIG = (1 << 63) - 1
-    while True:
-        go = torch.tensor([1], dtype=torch.int64, device=dev)
-        if rank == 0:
-            if time.monotonic() - start > config.t_max or (
-                    config.max_rounds is not None and rounds >= config.max_rounds):
-                go[0] = 0
-        dist.broadcast(go, src=0, group=group)
-        if int(go[0]) == 0:
-            break
+
+    def keep_going(done):   # rank 0's budget check before a round (gvns.py:197-199)
+        return not (time.monotonic() - start > config.t_max or (
+            config.max_rounds is not None and done >= config.max_rounds))
+
+    go = torch.tensor([1 if rank != 0 or keep_going(0) else 0], dtype=torch.int64, device=dev)
+    dist.broadcast(go, src=0, group=group)
+    going = int(go[0]) == 1
+    while going:
         cost, w, plan = be.round(rounds, strength)
         if local == 0:
             cost, w = BIG, BIG
-        mine = torch.tensor([cost, w], dtype=torch.int64, device=dev)
-        allb = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(world)]
+        # one all-gather per round: (cost, global worker) of every rank, and
+        # rank 0's budget decision for the next round rides along
+        nxt = 1 if rank != 0 or keep_going(rounds + 1) else 0
+        mine = torch.tensor([cost, w, nxt], dtype=torch.int64, device=dev)
+        allb = [torch.zeros(3, dtype=torch.int64, device=dev) for _ in range(world)]
         dist.all_gather(allb, mine, group=group)
-        pairs = [tuple(int(x) for x in t.tolist()) for t in allb]
+        rows = [t.tolist() for t in allb]
+        going = int(rows[0][2]) == 1
+        pairs = [(int(r[0]), int(r[1])) for r in rows]
         best_cost, best_w = min(pairs)
         src = min(r for r in range(world) if pairs[r] == (best_cost, best_w))
         improved = best_cost < inc_cost
