@@ -64,7 +64,7 @@ int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uint8_t *sr);
  * Bit 1: T > 63 never uses one CTA per product (by default
  * a CTA per product is used when K <= 2 x SMs, a warp per product above).
  * Bits 2/3: T <= 63 slack skip always / never (default: per launch). */
-int rl_instance_set_variant(rl_instance *h, int packed);
+int rl_instance_set_variant(rl_instance *h, int variant);
 /* info[0..5] = K, T, bytes per period value (4|8), bytes per cost (4|8),
  * SM count, warps per CTA of the resident VND kernel. */
 int rl_instance_info(const rl_instance *h, int64_t *info);

@@ -165,10 +165,11 @@ class DeviceInstance:
             _lib.rl_instance_destroy(h)
             self.h = None
 
-    def set_variant(self, packed):
-        """Kernel variant bits (identical results): 1 = two products per warp
-        for T <= 63, 2 = warp (not CTA) per product for T > 63; 0 = default."""
-        check(load().rl_instance_set_variant(self.h, int(packed)), "rl_instance_set_variant")
+    def set_variant(self, variant):
+        """Kernel variant bits (identical results; A/B and tests): 2 = warp
+        (not CTA) per product for T > 63; 4 / 8 = slack skip always / never
+        for T <= 63; 0 = default (chosen per launch)."""
+        check(load().rl_instance_set_variant(self.h, int(variant)), "rl_instance_set_variant")
 
     @property
     def launches(self):

@@ -1008,13 +1008,13 @@ static int launch_cfg_cta(rl_instance *h, const void *fn, int64_t nprod, int &gr
     return 0;
 }
 
-extern "C" int rl_instance_set_variant(rl_instance *h, int packed)
+extern "C" int rl_instance_set_variant(rl_instance *h, int variant)
 {
     // bit 0 (two products per warp) was removed: measured slower
-    if (!h || packed < 0 || packed > 11 || (packed & 12) == 12 || (packed & 1))
+    if (!h || variant < 0 || variant > 11 || (variant & 12) == 12 || (variant & 1))
         return fail(RL_EINVAL, "rl_instance_set_variant: bad arguments");
-    h->cta_long = (packed & 2) == 0;
-    h->skip_mode = (packed & 4) ? 1 : (packed & 8) ? 2 : 0;
+    h->cta_long = (variant & 2) == 0;
+    h->skip_mode = (variant & 4) ? 1 : (variant & 8) ? 2 : 0;
     return 0;
 }
 

@@ -77,10 +77,10 @@ def test_scan_products_golden(small_cases):
             assert ev == oev
 
 
-@pytest.mark.parametrize("packed", [8, 4])
-def test_vnd_golden(small_cases, packed):
+@pytest.mark.parametrize("variant", [8, 4])
+def test_vnd_golden(small_cases, variant):
     for inst, dev, p in _cases(small_cases):
-        dev.set_variant(packed)
+        dev.set_variant(variant)
         for k_max in (1, 4):
             sm, sr, trace, st = dev.vnd(small_cases[p + "sm"], small_cases[p + "sr"], k_max)
             assert st["cost"] == int(small_cases[p + f"vnd{k_max}_cost"]), p
@@ -138,14 +138,14 @@ def test_c1_every_lockstep_pass():
     assert st["sweeps"] == int(g["sweeps"]) == 45
 
 
-@pytest.mark.parametrize("packed", [8, 4])
-def test_k1000_vnd_golden(packed):
+@pytest.mark.parametrize("variant", [8, 4])
+def test_k1000_vnd_golden(variant):
     g = golden("k1000.npz")
     inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
     start = initial_solution(inst)
     np.testing.assert_array_equal(np.packbits(start.setup_m, axis=1), g["start_sm"])
     dev = DeviceInstance(inst)
-    dev.set_variant(packed)
+    dev.set_variant(variant)
     sm, sr, trace, st = dev.vnd(start.setup_m, start.setup_r)
     assert st["cost"] == int(g["cost"]) == 4484593955
     np.testing.assert_array_equal(trace, g["trace"])
@@ -160,8 +160,8 @@ def _big():
         return json.load(f)
 
 
-@pytest.mark.parametrize("packed", [8, 4])
-def test_c3_k100000_vnd_golden(packed):
+@pytest.mark.parametrize("variant", [8, 4])
+def test_c3_k100000_vnd_golden(variant):
     """BASELINE config 3 at full size: K=100,000, T=52 -- final cost
     449,100,704,810, full trace and plan hash from the live reference."""
     g = _big()["k100000_t52"]
@@ -169,7 +169,7 @@ def test_c3_k100000_vnd_golden(packed):
     start = initial_solution(inst)
     assert _plan_sha(start.setup_m, start.setup_r) == g["start_plan_sha"]
     dev = DeviceInstance(inst)
-    dev.set_variant(packed)
+    dev.set_variant(variant)
     sm, sr, trace, st = dev.vnd(start.setup_m, start.setup_r)
     assert st["cost"] == g["cost"] == 449100704810
     assert trace.tolist() == g["trace"]
@@ -213,16 +213,16 @@ def _random_instance(rng, K, T, big=False):
     return Instance(K, T, dem, ret, *c)
 
 
-@pytest.mark.parametrize("packed", [8, 4, 2, 0])
+@pytest.mark.parametrize("variant", [8, 4, 2, 0])
 @pytest.mark.parametrize("seed", range(12))
-def test_fuzz_against_oracle(seed, packed):
+def test_fuzz_against_oracle(seed, variant):
     rng = np.random.default_rng(1000 + seed)
     T = int(rng.choice([1, 2, 3, 5, 8, 31, 32, 33, 52, 63, 64, 65, 100, 150]))
     K = int(rng.integers(1, 60))
     big = seed % 4 == 3
     inst = _random_instance(rng, K, T, big)
     dev = DeviceInstance(inst)
-    dev.set_variant(packed)
+    dev.set_variant(variant)
     plans = [initial_solution(inst)]
     plans.append(type(plans[0])(rng.random((K, T)) < 0.5, rng.random((K, T)) < 0.3))
     plans.append(type(plans[0])(np.ones((K, T), bool), rng.random((K, T)) < 0.5))
