@@ -1249,8 +1249,11 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
     // waves of resident warps (C2, GVNS) -- measured, DESIGN.md section 5
     const bool skip = std::is_same<Mask, MaskReg>::value &&
                       (h->skip_mode == 1 || (h->skip_mode == 0 && nprod < (int64_t)h->sms * 64));
+    // the slack skip exists for register rows only: Skip=true is never
+    // instantiated for shared-memory rows
+    constexpr bool kReg = std::is_same<Mask, MaskReg>::value;
     const void *fn = cta ? (const void *)k_vnd_cta<V, C>
-                     : skip ? (const void *)k_vnd<V, C, Mask, true>
+                     : skip ? (const void *)k_vnd<V, C, Mask, kReg>
                             : (const void *)k_vnd<V, C, Mask, false>;
     int rc = cta ? launch_cfg_cta<V, C>(h, fn, nprod, grid, smem)
                  : launch_cfg<V, C>(h, fn, nprod, grid, smem, block);
@@ -1261,8 +1264,8 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
         k_vnd_cta<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
                                                                 sr_out, k_max, o);
     else if (skip)
-        k_vnd<V, C, Mask, true><<<grid, block, smem, st>>>(view<V>(h), sm_in, sr_in,
-                                                                        sm_out, sr_out, k_max, o);
+        k_vnd<V, C, Mask, kReg><<<grid, block, smem, st>>>(view<V>(h), sm_in, sr_in,
+                                                            sm_out, sr_out, k_max, o);
     else
         k_vnd<V, C, Mask, false><<<grid, block, smem, st>>>(view<V>(h), sm_in, sr_in,
                                                                          sm_out, sr_out, k_max, o);
