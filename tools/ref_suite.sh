@@ -1,0 +1,41 @@
+#!/bin/bash
+# Run the reference's own test suite, unchanged, against the B200 drop-in.
+#
+#   tools/ref_suite.sh stage   # here (needs /root/reference): copy the
+#                              # reference's tests into baseline/_ref/tests
+#                              # (git-ignored, travels to the GPU box)
+#   tools/ref_suite.sh run     # on a B200 box: pytest those files with
+#                              # `import remlot` resolved to the drop-in
+#                              # (paper_1704_05132_b200/compat/remlot)
+#
+# Staged: the model / plan / vnd / gvns / oracle tests and their helpers
+# (conftest.py, reference.py).  Not staged: test_cli.py, test_bench.py and
+# test_acceptance.py, which import the reference's CLI and bench/report
+# emitters (out of scope); the acceptance criteria on the path
+# (C3-C6) are covered by tests/test_gpu_parity.py against the goldens.
+set -e
+root=$(cd "$(dirname "$0")/.." && pwd)
+dst=$root/baseline/_ref/tests
+case "$1" in
+stage)
+  src=/root/reference/pkg/tests
+  mkdir -p "$dst"
+  rm -rf "$dst"
+  mkdir -p "$dst"
+  for f in conftest.py reference.py test_model.py test_plan.py test_vnd.py test_gvns.py \
+           test_oracle.py; do
+    cp "$src/$f" "$dst/$f"
+  done
+  echo "staged $(ls "$dst" | wc -l) files into $dst"
+  ;;
+run)
+  shift
+  cd "$root/baseline/_ref"
+  PYTHONPATH=$root/paper_1704_05132_b200/compat:$root${PYTHONPATH:+:$PYTHONPATH} \
+    python -m pytest tests -q -p no:cacheprovider "$@"
+  ;;
+*)
+  echo "usage: $0 stage|run [pytest args]" >&2
+  exit 2
+  ;;
+esac
