@@ -116,12 +116,20 @@ __device__ inline void stage_end(const Slot<V, C> &s, const InstView<V> &in, int
 
 // --------------------------------------------------------------- kernels
 
+// Largest per-period cost coefficient of product k (seg_cost's a0 - u h_M,
+// b0 + u h_R, k_M, k_R in magnitude): below 2^30 the int32-value /
+// int64-cost kernels multiply in 32 x 32 -> 64 bits (seg_cost<int32, int64>).
+__device__ inline double coef_bound(const double *c, int T)
+{
+    return fmax(fmax(c[4] + (double)T * c[2], c[5] + c[4] + (double)T * c[3]), fmax(c[0], c[1]));
+}
+
 __global__ void k_bounds(int64_t K, int T, const int64_t *dem, const int64_t *ret,
                          const int64_t *c6, unsigned long long *out /* [sumDR, B] as double bits */,
-                         int *negative)
+                         unsigned long long *qmax /* coef_bound, double bits */, int *negative)
 {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    double sdr = 0.0, B = 0.0;
+    double sdr = 0.0, B = 0.0, Q = 0.0;
     if (k < K) {
         double sd = 0.0, sr = 0.0;
         bool neg = false;
@@ -142,9 +150,11 @@ __global__ void k_bounds(int64_t K, int T, const int64_t *dem, const int64_t *re
         // upper bound of any plan's cost and of every intermediate term
         B = (double)T * (c[0] + c[1]) + (c[4] + c[5]) * sd + (double)T * c[2] * sd +
             (double)T * c[3] * sr;
+        Q = coef_bound(c, T);
     }
     atomicMax(&out[0], (unsigned long long)__double_as_longlong(sdr));
     atomicMax(&out[1], (unsigned long long)__double_as_longlong(B));
+    atomicMax(qmax, (unsigned long long)__double_as_longlong(Q));
 }
 
 template <typename V>
@@ -787,20 +797,21 @@ static int ensure_trace(rl_instance *h, int64_t cap_sweeps, int k_max)
 static int prepare(rl_instance *h)
 {
     const size_t kt = (size_t)h->K * h->T;
-    CK(cudaMemsetAsync(h->bounds, 0, 3 * sizeof(unsigned long long), h->stream));
+    CK(cudaMemsetAsync(h->bounds, 0, 4 * sizeof(unsigned long long), h->stream));
     CK(cudaMemsetAsync(h->ints, 0, 4 * sizeof(int), h->stream));
     const int blk = 256;
     k_bounds<<<(unsigned)((h->K + blk - 1) / blk), blk, 0, h->stream>>>(
-        h->K, h->T, h->dem64, h->ret64, h->cost6, h->bounds, h->ints + 2);
+        h->K, h->T, h->dem64, h->ret64, h->cost6, h->bounds, h->bounds + 3, h->ints + 2);
     CKL();
-    unsigned long long hb[2];
+    unsigned long long hb[4];
     int neg = 0;
     CK(cudaMemcpyAsync(hb, h->bounds, sizeof hb, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(&neg, h->ints + 2, sizeof neg, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    double sdr, B;
+    double sdr, B, Q;
     memcpy(&sdr, &hb[0], 8);
     memcpy(&B, &hb[1], 8);
+    memcpy(&Q, &hb[3], 8);
     if (neg)
         return fail(RL_ERANGE, "instance has negative entries (validate_instance rejects them)");
     if (!(sdr < std::ldexp(1.0, 60)) || !(B < std::ldexp(1.0, 61)))
@@ -808,7 +819,9 @@ static int prepare(rl_instance *h)
                     "instance too large for exact int64 costs (max sum D+R %.3g, cost bound %.3g)",
                     sdr, B);
     h->cost_bound = B;
-    const int vbytes = sdr < std::ldexp(1.0, 28) ? 4 : 8;
+    // int32 values only with int32 coefficients (seg_cost<int32, int64>
+    // multiplies 32 x 32 -> 64); int32 costs when every plan's cost fits
+    const int vbytes = sdr < std::ldexp(1.0, 28) && Q < std::ldexp(1.0, 30) ? 4 : 8;
     const int cbytes = (vbytes == 4 && B < std::ldexp(1.0, 30)) ? 4 : 8;
     if (h->dem && h->vbytes == 4 && vbytes != 4) {
         CK(cudaFree(h->dem));
@@ -1451,7 +1464,8 @@ __global__ void k_check_narrow(int64_t lo, int64_t hi, int T, int64_t K, const i
                              (double)T * c[2] * sd + (double)T * c[3] * sr;
             const double vlim = std::ldexp(1.0, vbytes == 4 ? 28 : 60);
             const double clim = std::ldexp(1.0, cbytes == 4 ? 30 : 61);
-            if (neg || !(sd + sr < vlim) || !(B < clim))
+            const bool qok = vbytes == 8 || coef_bound(c, T) < std::ldexp(1.0, 30);
+            if (neg || !(sd + sr < vlim) || !(B < clim) || !qok)
                 atomicExch(bad, 1);
             atomicMax(&bounds[0], (unsigned long long)__double_as_longlong(sd + sr));
             atomicMax(&bounds[1], (unsigned long long)__double_as_longlong(B));

@@ -511,6 +511,27 @@ __device__ inline bool seg_cost(V cdu, V cru, V cdv, int u, bool m, bool r, V X,
     return !(xm > 0 && !m);
 }
 
+// int32 values with int64 costs: the host selects this pair only when every
+// coefficient (p_M + T h_M, p_R + p_M + T h_R, k_M, k_R) is below 2^30
+// (prepare / k_check_narrow, coef_bound), so a0 - u h_M and b0 + u h_R are
+// exact in int32 and the two products are 32 x 32 -> 64 multiply-adds.
+template <>
+__device__ inline bool seg_cost<int32_t, int64_t>(int32_t cdu, int32_t cru, int32_t cdv, int u,
+                                                  bool m, bool r, int32_t X,
+                                                  const ProductCosts<int64_t> &pc, int64_t &c,
+                                                  int32_t &xr)
+{
+    const int32_t seg = cdv - cdu;
+    const int32_t avail = cru - X;
+    xr = r ? vmin(seg, avail) : 0;
+    const int32_t xm = seg - xr;
+    const int32_t ca = (int32_t)pc.a0 - u * (int32_t)pc.hm;
+    const int32_t cb = (int32_t)pc.b0 + u * (int32_t)pc.hr;
+    const int32_t setup = (xr > 0 ? (int32_t)pc.kr : 0) + (xm > 0 ? (int32_t)pc.km : 0);
+    c = (int64_t)seg * ca + (int64_t)xr * cb + setup;
+    return !(xm > 0 && !m);
+}
+
 // ------------------------------------------------------------ staging
 
 // Prefix sums of the staged rows into cd/cr; returns K0 (warp-uniform).

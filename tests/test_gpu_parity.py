@@ -293,6 +293,54 @@ def test_mixed_width_t520_paths(variant):
     np.testing.assert_array_equal(sm, om)
 
 
+@pytest.mark.parametrize("over", [False, True])
+@pytest.mark.parametrize("T", [52, 300])
+def test_int32_coefficient_bound(T, over):
+    """int32 values with int64 costs multiply in 32 x 32 -> 64 bits only
+    while every coefficient (p_M + T h_M, p_R + p_M + T h_R, k_M, k_R) is
+    below 2^30: at the bound the int32-value path is exact, one past it the
+    instance takes the int64-value path (coef_bound, remlot_b200.cu)."""
+    rng = np.random.default_rng(31 + T)
+    K = 8
+    dem = rng.integers(0, 101, size=(K, T))
+    dem[rng.random((K, T)) < 0.2] = 0
+    ret = (rng.random((K, T)) * dem * 0.5).astype(np.int64)
+    lim = 2**30 - 1
+    pm = rng.integers(0, 1000, size=K)
+    pr = rng.integers(0, 1000, size=K)
+    hm = (lim - pm) // T           # p_M + T h_M <= 2^30 - 1
+    hr = (lim - pm - pr) // T      # p_R + p_M + T h_R <= 2^30 - 1
+    km = np.full(K, lim)
+    kr = rng.integers(lim // 2, lim, size=K)
+    if over:
+        km[3] = lim + 1
+    inst = Instance(K, T, dem, ret, km, kr, hm, hr, pm, pr)
+    dev = DeviceInstance(inst)
+    assert dev.info["value_bytes"] == (8 if over else 4)
+    assert dev.info["cost_bytes"] == 8
+    start = initial_solution(inst)
+    sm, sr, trace, st = dev.vnd(start.setup_m, start.setup_r)
+    om, orr, ocost, otrace, ost = oracle.vnd(inst, start.setup_m, start.setup_r)
+    assert st["cost"] == ocost
+    np.testing.assert_array_equal(trace, otrace)
+    np.testing.assert_array_equal(sm, om)
+    np.testing.assert_array_equal(sr, orr)
+    assert st["evals_reference"] == ost["evals"]
+    np.testing.assert_array_equal(dev.product_costs(sm, sr),
+                                  oracle.product_costs(inst, sm, sr))
+    if over:
+        # streamed into a handle laid out for int32 values: the per-chunk
+        # check sees the coefficient and falls back to a full upload
+        small = generate_instance(GeneratorConfig(products=K, periods=T, seed=1))
+        dev2 = DeviceInstance(small)
+        assert dev2.info["value_bytes"] == 4
+        sm2, sr2, trace2, st2 = dev2.vnd_host(inst, start.setup_m, start.setup_r)
+        assert st2["cost"] == ocost
+        np.testing.assert_array_equal(trace2, otrace)
+        np.testing.assert_array_equal(sm2, om)
+        np.testing.assert_array_equal(sr2, orr)
+
+
 def test_c3_vnd_host_pipelined_golden():
     """rl_vnd_host (chunked uploads overlapped with the descent, the bench's
     e2e call) reproduces the C3 golden, then serves a different instance of
