@@ -306,10 +306,19 @@ struct MaskSmem {
     {
         const int L = (T + 31) >> 5;
         const int lo = lane * L, hi = min(lo + L, T);
+        // first setup in [lo, hi): scan the chunk's words
         int first = T;
-        for (int t = hi - 1; t >= lo; --t)
-            if (setup(t))
-                first = t;
+        if (lo < hi) {
+            int w = lo >> 5;
+            const int wl = (hi - 1) >> 5;
+            uint32_t bits = (bm[w] | br[w]) & (0xffffffffu << (lo & 31));
+            while (!bits && w < wl) {
+                ++w;
+                bits = bm[w] | br[w];
+            }
+            const int f = bits ? (w << 5) + __ffs(bits) - 1 : T;
+            first = f < hi ? f : T;
+        }
         int sf = first;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -322,13 +331,19 @@ struct MaskSmem {
             run = T;
         // the first setup >= hi (a lane's successor chunk) and its kind
         int ty = run < T ? (int)m(run) | (int)r(run) << 1 : 0;
-        for (int t = hi - 1; t >= lo; --t) {
-            const int k = (int)m(t) | (int)r(t) << 1;
-            if (k) {
-                run = t;
-                ty = k;
+        // descending over the chunk, one pair of word loads per 32 periods
+        for (int t = hi - 1; t >= lo;) {
+            const int w = t >> 5;
+            const uint32_t mw = bm[w], rw = br[w];
+            const int tl = max(lo, w << 5);
+            for (; t >= tl; --t) {
+                const int k = (int)((mw >> (t & 31)) & 1u) | (int)((rw >> (t & 31)) & 1u) << 1;
+                if (k) {
+                    run = t;
+                    ty = k;
+                }
+                nx[t] = (uint16_t)(run | ty << kTypeShift);
             }
-            nx[t] = (uint16_t)(run | ty << kTypeShift);
         }
         if (lane == 31)
             nx[T] = (uint16_t)T;
@@ -342,30 +357,35 @@ struct PatchedSmem {
     MaskSmem base;
     int a, b, ta, tb;
     // first setup >= x (T if none) and its kind
+    // (x <= T: nx[T] = T is the end entry)
     __device__ int next_t(int x, int &ty) const
     {
         const int T = base.T;
-        int e = x >= T ? T : base.nx[x];
+        int e = base.nx[x];
         int t = e & kPeriodMask;
         ty = e >> kTypeShift;
-        // base setups the move clears (at most a and b) are skipped
+        // past the move (x > b >= a) the rows are the base rows; most walk
+        // steps take only the lookup above
+        if (x <= b) {
+            // base setups the move clears (at most a and b) are skipped
 #pragma unroll 1
-        while (t < T && (t == a || t == b)) {
-            const int pt = t == a ? ta : tb;
-            if (pt) {
-                ty = pt;
-                break;
+            while (t < T && (t == a || t == b)) {
+                const int pt = t == a ? ta : tb;
+                if (pt) {
+                    ty = pt;
+                    break;
+                }
+                e = base.nx[t + 1];
+                t = e & kPeriodMask;
+                ty = e >> kTypeShift;
             }
-            e = t + 1 >= T ? T : base.nx[t + 1];
-            t = e & kPeriodMask;
-            ty = e >> kTypeShift;
-        }
-        if (x <= a && a < t && ta) {
-            t = a;
-            ty = ta;
-        } else if (x <= b && b < t && tb) {
-            t = b;
-            ty = tb;
+            if (x <= a && a < t && ta) {
+                t = a;
+                ty = ta;
+            } else if (b < t && tb) {
+                t = b;
+                ty = tb;
+            }
         }
         return t;
     }
