@@ -624,15 +624,33 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
     const int L = (T + 31) >> 5;
     const int lo = lane * L, hi = min(lo + L, T);
     const V INF = VInf<V>::value;
+    constexpr bool kSmem = std::is_same<Mask, MaskSmem>::value;
     V A = 0, B = INF;
-    for (int u = lo; u < hi; ++u) {
-        if (!mk.r(u))
-            continue;   // only remanufacturing setups move X
-        const int v = mk.next(u + 1);
-        const DR<V> e = s.dr[u];
-        const V seg = s.dr[v].d - e.d;
-        A += seg;
-        B = vmin<V>(B + seg, e.r);
+    if constexpr (kSmem) {
+        // setup to setup through the next-setup table (one 16-bit load per
+        // setup instead of two bit-row loads per period)
+        int e = lo < hi ? mk.nx[lo] : hi;
+        for (int u = e & kPeriodMask; u < hi;) {
+            const int e2 = mk.nx[u + 1], v = e2 & kPeriodMask;
+            if ((e >> kTypeShift) & 2) {   // only remanufacturing setups move X
+                const DR<V> d = s.dr[u];
+                const V seg = s.dr[v].d - d.d;
+                A += seg;
+                B = vmin<V>(B + seg, d.r);
+            }
+            u = v;
+            e = e2;
+        }
+    } else {
+        for (int u = lo; u < hi; ++u) {
+            if (!mk.r(u))
+                continue;   // only remanufacturing setups move X
+            const int v = mk.next(u + 1);
+            const DR<V> e = s.dr[u];
+            const V seg = s.dr[v].d - e.d;
+            A += seg;
+            B = vmin<V>(B + seg, e.r);
+        }
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -648,23 +666,41 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
     constexpr bool kSkip = Skip && std::is_same<Mask, MaskReg>::value;
     C local = 0;
     bool ok = true;
-    for (int u = lo; u < hi; ++u) {
-        const bool m = mk.m(u), r = mk.r(u);
-        if (kSkip)
-            s.slk[u] = INF;
-        if (!(m | r))
-            continue;
-        const int v = mk.next(u + 1);
-        const DR<V> e = s.dr[u];
-        const V cdv = s.dr[v].d;
-        s.xc.set(u, X, local);
-        if (kSkip && r)
-            s.slk[u] = e.r - X - (cdv - e.d);
-        C c;
-        V xr;
-        ok &= seg_cost<V, C>(e.d, e.r, cdv, u, m, r, X, pc, c, xr);
-        local += c;
-        X += xr;
+    if constexpr (kSmem) {
+        int e = lo < hi ? mk.nx[lo] : hi;
+        for (int u = e & kPeriodMask; u < hi;) {
+            const int e2 = mk.nx[u + 1], v = e2 & kPeriodMask;
+            const int ty = e >> kTypeShift;
+            const DR<V> d = s.dr[u];
+            const V cdv = s.dr[v].d;
+            s.xc.set(u, X, local);
+            C c;
+            V xr;
+            ok &= seg_cost<V, C>(d.d, d.r, cdv, u, ty & 1, ty >> 1, X, pc, c, xr);
+            local += c;
+            X += xr;
+            u = v;
+            e = e2;
+        }
+    } else {
+        for (int u = lo; u < hi; ++u) {
+            const bool m = mk.m(u), r = mk.r(u);
+            if (kSkip)
+                s.slk[u] = INF;
+            if (!(m | r))
+                continue;
+            const int v = mk.next(u + 1);
+            const DR<V> e = s.dr[u];
+            const V cdv = s.dr[v].d;
+            s.xc.set(u, X, local);
+            if (kSkip && r)
+                s.slk[u] = e.r - X - (cdv - e.d);
+            C c;
+            V xr;
+            ok &= seg_cost<V, C>(e.d, e.r, cdv, u, m, r, X, pc, c, xr);
+            local += c;
+            X += xr;
+        }
     }
     C incl = local;
 #pragma unroll
@@ -674,10 +710,17 @@ __device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
             incl += o;
     }
     const C excl = incl - local;
-    if (excl != C(0))
-        for (int u = lo; u < hi; ++u)
-            if (mk.m(u) | mk.r(u))
+    if (excl != C(0)) {
+        if constexpr (kSmem) {
+            for (int u = lo < hi ? mk.nx[lo] & kPeriodMask : hi; u < hi;
+                 u = mk.nx[u + 1] & kPeriodMask)
                 s.xc.add_c(u, excl);
+        } else {
+            for (int u = lo; u < hi; ++u)
+                if (mk.m(u) | mk.r(u))
+                    s.xc.add_c(u, excl);
+        }
+    }
     S = __shfl_sync(FULL, incl, 31);
     if (lane == 0)
         s.xc.set(T, V(0), S);   // end entry: a walk reaching T adds S - S
