@@ -168,15 +168,28 @@ int rl_decode(rl_instance *h, const uint8_t *sm, const uint8_t *sr, int64_t *x_m
  * 2^64 like gvns.py:89).  *inc_cost = evaluate(inc). */
 int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset, int k_max, int k_vnd_max,
                   uint64_t seed, const uint8_t *sm, const uint8_t *sr, int64_t *inc_cost);
+/* rl_gvns_begin with speculative batches of `batch` (1..32) rounds for
+ * rl_gvns_run: B x W worker slots; the round counter starts at 0. */
+int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64_t worker_offset, int k_max,
+                        int k_vnd_max, uint64_t seed, const uint8_t *sm, const uint8_t *sr,
+                        int64_t *inc_cost);
 /* Overwrite the shake strength k (worker_round(..., k, ...)). */
 int rl_gvns_set_strength(rl_instance *h, int64_t strength);
 /* One round (worker_round, gvns.py:147-174) with round index round_index;
  * accept = 1 also applies the GVNS step (gvns.py:207-215) on the device
  * (accept strict improvement, next_strength).  Asynchronous. */
 int rl_gvns_round(rl_instance *h, int64_t round_index, int accept);
+/* The gvns loop body (gvns.py:200-215) for up to `batch` rounds starting at
+ * the device round counter, never past max_rounds: every round of the batch
+ * shakes the incumbent with the strength it has if the rounds before it do
+ * not improve; the join applies the rounds in order and stops at the first
+ * accepted one (later rounds are re-run by the next call), so the result is
+ * the sequential trajectory.  Asynchronous; the counter is info[6]. */
+int rl_gvns_run(rl_instance *h, int64_t max_rounds);
 /* which = 0: incumbent, 1: last round's winning candidate (accept = 0).
- * info[0..5] = incumbent cost, strength, last best cost, last best worker,
- * accepted rounds, shake fallbacks in the last round.  sm/sr may be NULL. */
+ * info[0..6] = incumbent cost, strength, last best cost, last best worker,
+ * accepted rounds, shake fallbacks in the last round, rounds completed.
+ * sm/sr may be NULL. */
 int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr, int64_t *info);
 /* Sharded rounds (one rank per GPU, workers split in blocks): after
  * rl_gvns_round(h, r, 0), rl_gvns_candidate copies this rank's winning

@@ -24,8 +24,8 @@ EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_instance_info", "rl_product_costs", "rl_scan_products", "rl_apply_scan",
            "rl_list_moves", "rl_vnd", "rl_vnd_device", "rl_vnd_collect", "rl_vnd_host",
            "rl_vnd_product_stats",
-           "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_oracle_optimal", "rl_int_peak", "rl_gvns_begin", "rl_gvns_set_strength",
-           "rl_gvns_round", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
+           "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_oracle_optimal", "rl_int_peak", "rl_gvns_begin", "rl_gvns_begin_batch", "rl_gvns_set_strength",
+           "rl_gvns_round", "rl_gvns_run", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
            "rl_rng_probe", "rl_launch_count", "rl_generate_instance", "rl_instance_download",
            "rl_last_error")
 
@@ -70,6 +70,8 @@ def load():
         "rl_int_peak": (I, [P]),
         "rl_oracle_optimal": (I, [P, P, P, P]),
         "rl_gvns_begin": (I, [P, I, I64, I, I, ctypes.c_uint64, P, P, P]),
+        "rl_gvns_begin_batch": (I, [P, I, I, I64, I, I, ctypes.c_uint64, P, P, P]),
+        "rl_gvns_run": (I, [P, I64]),
         "rl_gvns_candidate": (I, [P, P, P]),
         "rl_gvns_import": (I, [P, P, I64]),
         "rl_gvns_set_strength": (I, [P, I64]),
@@ -277,13 +279,17 @@ class DeviceInstance:
         return outs[0], outs[1], outs[2], outs[3], cost
 
     # ---- device GVNS (gvns_impl.cuh)
-    def gvns_begin(self, workers, k_max, k_vnd_max, seed, sm, sr, worker_offset=0):
+    def gvns_begin(self, workers, k_max, k_vnd_max, seed, sm, sr, worker_offset=0, batch=1):
         sm, sr = u8(sm), u8(sr)
         cost = np.zeros(1, np.int64)
-        check(load().rl_gvns_begin(self.h, workers, worker_offset, k_max, k_vnd_max,
-                                   seed & ((1 << 64) - 1), ptr(sm), ptr(sr), ptr(cost)),
+        check(load().rl_gvns_begin_batch(self.h, workers, batch, worker_offset, k_max, k_vnd_max,
+                                         seed & ((1 << 64) - 1), ptr(sm), ptr(sr), ptr(cost)),
               "rl_gvns_begin")
         return int(cost[0])
+
+    def gvns_run(self, max_rounds):
+        """One speculative batch of rounds at the device round counter."""
+        check(load().rl_gvns_run(self.h, max_rounds), "rl_gvns_run")
 
     def gvns_candidate(self, d_plan_ptr):
         """(cost, global worker) of this rank's best candidate; copies the plan
@@ -304,7 +310,7 @@ class DeviceInstance:
 
     def gvns_state(self, which, want_plan=True):
         """which 0 = incumbent, 1 = last candidate -> (sm, sr, info dict)."""
-        info = np.zeros(6, np.int64)
+        info = np.zeros(7, np.int64)
         sm = sr = None
         if want_plan:
             sm = np.empty((self.K, self.T), np.bool_)
@@ -314,7 +320,8 @@ class DeviceInstance:
               "rl_gvns_state")
         return sm, sr, dict(inc_cost=int(info[0]), strength=int(info[1]),
                             best_cost=int(info[2]), best_worker=int(info[3]),
-                            accepted=int(info[4]), fallbacks=int(info[5]))
+                            accepted=int(info[4]), fallbacks=int(info[5]),
+                            rounds=int(info[6]))
 
     def oracle_optimal(self):
         """Exhaustive per-product optimum (T <= 10): (costs, sm, sr)."""

@@ -13,11 +13,21 @@
 //   k_gvns_vnd        warp per (worker, touched product) [+ fallback plans]
 //   k_gvns_join       block: min (cost, worker) join, accept, next strength
 // with no host synchronisation; the incumbent and F stay resident.
+//
+// Speculative batches (rl_gvns_begin_batch / rl_gvns_run): rounds r0 ..
+// r0+B-1 run as one launch of B x W worker slots, each round shaking the
+// same incumbent with the strength it would have if no earlier round of the
+// batch improved (the round's RNG streams depend only on (seed, round, w)).
+// The join walks the rounds in order and stops at the first accepted one;
+// the rounds after it are discarded and re-run from the new incumbent by the
+// next batch, so the trajectory is exactly the sequential one.  Most rounds
+// do not improve, and a batch costs about one round's latency.
 
 struct GvnsArgs {
     int64_t K, KT, pop;
     int64_t w0;                       // global index of local worker 0 (sharded rounds)
     int T, NW, W, k_max, kcap, tcap, tsize, fb_slots;
+    int Wr, B;                        // workers per round, rounds per batch (W = B x Wr slots)
     int shake_bytes;                  // per-worker shared scratch of k_shake (0: global)
     uint64_t seed;
     uint8_t *inc, *F, *init, *cand;   // 2KT bytes each: m rows then r rows
@@ -47,8 +57,34 @@ enum {
     GV_ACCEPTED,
     GV_FB_COUNT,
     GV_ERROR,
+    GV_ROUND,     // rounds completed (the next batch starts here)
+    GV_NB,        // rounds of the next batch (adaptive, <= B)
     GV_FBCOST0,   // fb_slots entries follow
 };
+
+// Rounds of this launch: round_arg >= 0 names the first round (single-round
+// calls), else the device counter does; at most GV_NB (the adaptive batch
+// size: 1 after an accepted round, doubled up to B after a batch without
+// one, so improving phases run round by round and stagnating phases
+// speculate) and never past max_rounds.
+__device__ inline int gv_batch(const GvnsArgs &g, int64_t round_arg, int64_t max_rounds,
+                               int64_t &r0)
+{
+    r0 = round_arg >= 0 ? round_arg : g.scal[GV_ROUND];
+    const int64_t cap = round_arg >= 0 ? g.B : g.scal[GV_NB];
+    const int64_t left = max_rounds - r0;
+    return left <= 0 ? 0 : left < cap ? (int)left : (int)cap;
+}
+
+// Strength of batch round j if rounds 0..j-1 do not improve
+// (next_strength, gvns.py:177-181, applied j times).
+__device__ inline int64_t gv_strength(const GvnsArgs &g, int j)
+{
+    int64_t k = g.scal[GV_STRENGTH];
+    for (int i = 0; i < j; ++i)
+        k = k >= g.k_max ? 1 : k + 1;
+    return k;
+}
 
 // The same test segment by segment over prefix sums cd[t] = sum_{i<t} D,
 // cr[t] = sum_{i<t} R (closed form of DESIGN.md 3: x_R = min(seg, cr[u+1] -
@@ -121,7 +157,7 @@ __device__ inline bool row_feasible(const V *d, const V *r, int T, BitM bm, BitR
 // (incumbent bits, demand, returns) into L1 with coalesced loads first, so
 // lane 0's sequential feasibility walk hits the cache instead of DRAM/L2.
 template <typename V>
-__global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
+__global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t max_rounds)
 {
     extern __shared__ __align__(16) unsigned char shk[];
     const int lane = threadIdx.x & 31;
@@ -140,10 +176,20 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round)
     }
     if (w >= g.W)
         return;
+    int64_t r0;
+    const int nb = gv_batch(g, round_arg, max_rounds, r0);
+    const int jr = w / g.Wr;   // batch round of this slot
+    if (jr >= nb) {            // past the batch: no tasks, no fallback
+        if (lane == 0) {
+            g.tn[w] = 0;
+            g.fb[w] = 0;
+        }
+        return;
+    }
     Philox rng;
     if (lane == 0)
-        rng.seed(g.seed, (uint64_t)round, (uint64_t)(g.w0 + w));
-    const int64_t strength = g.scal[GV_STRENGTH];
+        rng.seed(g.seed, (uint64_t)(r0 + jr), (uint64_t)(g.w0 + w % g.Wr));
+    const int64_t strength = gv_strength(g, jr);
     const int64_t k_eff = strength < g.pop ? strength : g.pop;   // gvns.py:113
     const int T = g.T, NW = g.NW;
     // the draw's scratch (Floyd table, positions, touched rows) lives in
@@ -319,7 +365,7 @@ __global__ void k_shake_fallback(InstView<V> in, GvnsArgs g)
     Philox rng;
     rng.st = g.rng[w];
     rng.shuffle(diff, n);
-    const int64_t strength = g.scal[GV_STRENGTH];
+    const int64_t strength = gv_strength(g, w / g.Wr);
     const int64_t k_eff = strength < g.pop ? strength : g.pop;
     for (int64_t k = 0; k < K; ++k)
         bad[k] = 0;   // the incumbent is feasible
@@ -431,68 +477,126 @@ __global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, in
     }
 }
 
+// Candidate cost of worker slot w: F's total with its touched products'
+// re-descended costs, or its fallback plan's cost.
+__device__ inline long long gv_worker_cost(const GvnsArgs &g, int w)
+{
+    if (g.fb[w]) {
+        const int slot = g.fbslot[w];
+        return slot < g.fb_slots ? g.scal[GV_FBCOST0 + slot] : 0x7fffffffffffffffll;
+    }
+    long long c = g.scal[GV_FTOT];
+    for (int j = 0; j < g.tn[w]; ++j) {
+        c -= g.Fcost[g.tp[(int64_t)w * g.tcap + j]];
+        c += g.tcost[(int64_t)w * g.tcap + j];
+    }
+    return c;
+}
+
 // Join (gvns.py:170-174: min cost, lowest worker on ties) and, in accept
 // mode, the GVNS step (gvns.py:207-215): accept strict improvements, reset or
 // advance the strength (next_strength, gvns.py:177-181).  mode 0 writes the
-// winning candidate plan to g.cand (worker_round's return value).
-__global__ void k_gvns_join(GvnsArgs g, int mode)
+// winning candidate plan to g.cand (worker_round's return value).  A batch
+// (B > 1, accept mode) joins each round with one warp and applies the steps
+// in round order up to the first acceptance (GV_ROUND advances by the rounds
+// used).
+__global__ void k_gvns_join(GvnsArgs g, int mode, int64_t round_arg, int64_t max_rounds)
 {
     __shared__ long long s_cost[32];
     __shared__ int s_w[32];
-    __shared__ int s_accept;
+    __shared__ int s_accept, s_win;
+    int64_t r0;
+    const int nb = gv_batch(g, round_arg, max_rounds, r0);
+    if (nb == 0)
+        return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    long long best = 0x7fffffffffffffffll;
-    int bw = 0x7fffffff;
-    for (int w = tid; w < g.W; w += blockDim.x) {
-        long long c;
-        if (g.fb[w]) {
-            const int slot = g.fbslot[w];
-            c = slot < g.fb_slots ? g.scal[GV_FBCOST0 + slot] : 0x7fffffffffffffffll;
-        } else {
-            c = g.scal[GV_FTOT];
-            for (int j = 0; j < g.tn[w]; ++j) {
-                c -= g.Fcost[g.tp[(int64_t)w * g.tcap + j]];
-                c += g.tcost[(int64_t)w * g.tcap + j];
+    const int nwarps = (int)(blockDim.x >> 5);
+    if (g.B == 1) {
+        long long best = 0x7fffffffffffffffll;
+        int bw = 0x7fffffff;
+        for (int w = tid; w < g.W; w += blockDim.x) {
+            const long long c = gv_worker_cost(g, w);
+            if (c < best || (c == best && w < bw)) {
+                best = c;
+                bw = w;
             }
         }
-        if (c < best || (c == best && w < bw)) {
-            best = c;
-            bw = w;
+        for (int off = 16; off; off >>= 1) {
+            const long long oc = __shfl_xor_sync(FULL, best, off);
+            const int ow = __shfl_xor_sync(FULL, bw, off);
+            if (oc < best || (oc == best && ow < bw)) {
+                best = oc;
+                bw = ow;
+            }
         }
-    }
-    for (int off = 16; off; off >>= 1) {
-        const long long oc = __shfl_xor_sync(FULL, best, off);
-        const int ow = __shfl_xor_sync(FULL, bw, off);
-        if (oc < best || (oc == best && ow < bw)) {
-            best = oc;
-            bw = ow;
+        if (lane == 0) {
+            s_cost[wid] = best;
+            s_w[wid] = bw;
         }
-    }
-    if (lane == 0) {
-        s_cost[wid] = best;
-        s_w[wid] = bw;
+        __syncthreads();
+        if (tid == 0)
+            for (int i = 1; i < nwarps; ++i)
+                if (s_cost[i] < s_cost[0] || (s_cost[i] == s_cost[0] && s_w[i] < s_w[0])) {
+                    s_cost[0] = s_cost[i];
+                    s_w[0] = s_w[i];
+                }
+    } else {
+        // warp per batch round (B <= 32): slots j*Wr .. j*Wr + Wr - 1
+        for (int jr = wid; jr < nb; jr += nwarps) {
+            long long best = 0x7fffffffffffffffll;
+            int bw = 0x7fffffff;
+            for (int q = lane; q < g.Wr; q += 32) {
+                const int w = jr * g.Wr + q;
+                const long long c = gv_worker_cost(g, w);
+                if (c < best || (c == best && w < bw)) {
+                    best = c;
+                    bw = w;
+                }
+            }
+            for (int off = 16; off; off >>= 1) {
+                const long long oc = __shfl_xor_sync(FULL, best, off);
+                const int ow = __shfl_xor_sync(FULL, bw, off);
+                if (oc < best || (oc == best && ow < bw)) {
+                    best = oc;
+                    bw = ow;
+                }
+            }
+            if (lane == 0) {
+                s_cost[jr] = best;
+                s_w[jr] = bw;
+            }
+        }
     }
     __syncthreads();
     if (tid == 0) {
-        for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
-            if (s_cost[i] < s_cost[0] || (s_cost[i] == s_cost[0] && s_w[i] < s_w[0])) {
-                s_cost[0] = s_cost[i];
-                s_w[0] = s_w[i];
-            }
-        g.scal[GV_BEST_COST] = s_cost[0];
-        g.scal[GV_BEST_W] = g.w0 + s_w[0];
-        int acc = 0;
+        int acc = 0, win = 0, used = nb;
         if (mode == 1) {
-            acc = s_cost[0] < g.scal[GV_INC_COST];
-            const int64_t k = g.scal[GV_STRENGTH];
-            g.scal[GV_STRENGTH] = (acc || k >= g.k_max) ? 1 : k + 1;
+            int64_t k = g.scal[GV_STRENGTH];
+            for (int jr = 0; jr < nb; ++jr) {
+                win = jr;
+                acc = s_cost[jr] < g.scal[GV_INC_COST];
+                k = (acc || k >= g.k_max) ? 1 : k + 1;
+                if (acc) {
+                    used = jr + 1;
+                    break;
+                }
+            }
+            g.scal[GV_STRENGTH] = k;
         }
+        g.scal[GV_BEST_COST] = s_cost[win];
+        g.scal[GV_BEST_W] = g.w0 + s_w[win] % g.Wr;
+        g.scal[GV_ROUND] = r0 + used;
+        if (round_arg < 0)
+            g.scal[GV_NB] = acc ? 1 : (2 * nb < g.B ? 2 * nb : g.B);
         s_accept = mode == 0 ? 1 : acc;
+        s_win = win;
     }
     __syncthreads();
-    const int w = s_w[0];
+    const int win = s_win;
     if (!s_accept)
         return;
+    const int w = s_w[win];
+    const long long wcost = s_cost[win];
     // the candidate: F with the winner's touched rows, or its fallback plan
     uint8_t *dst = mode == 0 ? g.cand : g.inc;
     const int64_t KT2 = 2 * g.KT;
@@ -530,8 +634,8 @@ __global__ void k_gvns_join(GvnsArgs g, int mode)
     }
     __syncthreads();
     if (mode == 1 && tid == 0) {
-        g.scal[GV_INC_COST] = s_cost[0];
-        g.scal[GV_FTOT] = s_cost[0];
+        g.scal[GV_INC_COST] = wcost;
+        g.scal[GV_FTOT] = wcost;
         g.scal[GV_INC_IS_F] = 1;
         g.scal[GV_ACCEPTED] += 1;
     }
@@ -586,32 +690,36 @@ static int gv_launch_vnd(rl_instance *h, GvnsState *gs)
 }
 
 template <typename V, typename C>
-static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round)
+static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round_arg,
+                           int64_t max_rounds)
 {
     const int W = gs->a.W;
-    k_shake<V><<<(W + 3) / 4, 128, 4 * (size_t)gs->a.shake_bytes, h->stream>>>(view<V>(h), gs->a,
-                                                                            round);
+    k_shake<V><<<(W + 3) / 4, 128, 4 * (size_t)gs->a.shake_bytes, h->stream>>>(
+        view<V>(h), gs->a, round_arg, max_rounds);
     CKL();
     k_shake_fallback<V><<<(W + 63) / 64, 64, 0, h->stream>>>(view<V>(h), gs->a);
     CKL();
     return 0;
 }
 
-extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset, int k_max,
-                             int k_vnd_max, uint64_t seed, const uint8_t *sm, const uint8_t *sr,
-                             int64_t *inc_cost)
+extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64_t worker_offset,
+                                   int k_max, int k_vnd_max, uint64_t seed, const uint8_t *sm,
+                                   const uint8_t *sr, int64_t *inc_cost)
 {
     (void)cudaGetLastError();
-    if (!h || !sm || !sr || workers < 1 || worker_offset < 0 || k_max < 1 || k_vnd_max < 1 ||
-        k_vnd_max > 4)
-        return fail(RL_EINVAL, "rl_gvns_begin: bad arguments (workers=%d k_max=%d k_vnd_max=%d)",
-                    workers, k_max, k_vnd_max);
+    if (!h || !sm || !sr || workers < 1 || batch < 1 || batch > 32 ||
+        (int64_t)workers * batch > (1 << 20) || worker_offset < 0 || k_max < 1 ||
+        k_vnd_max < 1 || k_vnd_max > 4)
+        return fail(RL_EINVAL,
+                    "rl_gvns_begin: bad arguments (workers=%d batch=%d k_max=%d k_vnd_max=%d)",
+                    workers, batch, k_max, k_vnd_max);
+    const int slots = workers * batch;
     CK(cudaSetDevice(h->device));
     const int64_t K = h->K, KT = K * h->T, pop = 2 * KT;
     const int T = h->T, NW = (T + 31) / 32;
     const int64_t keff_max = k_max < pop ? k_max : pop;
     GvnsState *gs = h->gv;
-    const bool reuse = gs && gs->a.W == workers && gs->a.k_max == k_max;
+    const bool reuse = gs && gs->a.Wr == workers && gs->a.B == batch && gs->a.k_max == k_max;
     if (!reuse) {
         gvns_free(gs);
         h->gv = gs = new GvnsState();
@@ -621,7 +729,9 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset,
         a.pop = pop;
         a.T = T;
         a.NW = NW;
-        a.W = workers;
+        a.W = slots;
+        a.Wr = workers;
+        a.B = batch;
         a.k_max = k_max;
         a.kcap = (int)keff_max;
         a.tcap = (int)(keff_max < K ? keff_max : K);
@@ -635,8 +745,8 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset,
         const double per_slot = (double)pop * (1 + 8) + 8.0 * K;
         int fbs = (int)(512.0 * (1 << 20) / per_slot);
         fbs = fbs < 1 ? 1 : fbs;
-        fbs = fbs > workers ? workers : fbs;
-        a.fb_slots = fbs > 64 && workers > 64 ? 64 : fbs;
+        fbs = fbs > slots ? slots : fbs;
+        a.fb_slots = fbs > 64 && slots > 64 ? 64 : fbs;
         cudaError_t e = gv_alloc(gs, &a.inc, 4 * (size_t)pop);
         if (e == cudaSuccess) {
             a.F = a.inc + pop;
@@ -645,19 +755,19 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset,
             e = gv_alloc(gs, &a.Fcost, K * 8);
         }
         if (e == cudaSuccess) e = gv_alloc(gs, &a.scal, (GV_FBCOST0 + a.fb_slots) * 8);
-        if (e == cudaSuccess) e = gv_alloc(gs, &a.pos, (size_t)workers * a.kcap * 8);
-        if (e == cudaSuccess) e = gv_alloc(gs, &a.table, (size_t)workers * a.tsize * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.pos, (size_t)slots * a.kcap * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.table, (size_t)slots * a.tsize * 8);
         if (e == cudaSuccess && choice_uses_tail_shuffle(pop, keff_max))
-            e = gv_alloc(gs, &a.tailidx, (size_t)workers * pop * 8);
-        if (e == cudaSuccess) e = gv_alloc(gs, &a.tp, (size_t)workers * a.tcap * 8);
-        if (e == cudaSuccess) e = gv_alloc(gs, &a.tn, (size_t)workers * 3 * sizeof(int));
+            e = gv_alloc(gs, &a.tailidx, (size_t)slots * pop * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.tp, (size_t)slots * a.tcap * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.tn, (size_t)slots * 3 * sizeof(int));
         if (e == cudaSuccess) {
-            a.fb = a.tn + workers;
-            a.fbslot = a.fb + workers;
-            e = gv_alloc(gs, &a.tw, (size_t)workers * a.tcap * 2 * NW * 4);
+            a.fb = a.tn + slots;
+            a.fbslot = a.fb + slots;
+            e = gv_alloc(gs, &a.tw, (size_t)slots * a.tcap * 2 * NW * 4);
         }
-        if (e == cudaSuccess) e = gv_alloc(gs, &a.tcost, (size_t)workers * a.tcap * 8);
-        if (e == cudaSuccess) e = gv_alloc(gs, &a.rng, (size_t)workers * sizeof(PhiloxState));
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.tcost, (size_t)slots * a.tcap * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.rng, (size_t)slots * sizeof(PhiloxState));
         if (e == cudaSuccess) e = gv_alloc(gs, &a.fbplan, (size_t)a.fb_slots * pop);
         if (e == cudaSuccess) e = gv_alloc(gs, &a.fbdiff, (size_t)a.fb_slots * pop * 8);
         if (e == cudaSuccess) e = gv_alloc(gs, &a.fbpcost, (size_t)a.fb_slots * K * 8);
@@ -692,11 +802,21 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset,
     scal[GV_FTOT] = sum[0];
     scal[GV_STRENGTH] = 1;
     scal[GV_INC_IS_F] = 0;
+    scal[GV_ROUND] = 0;
+    scal[GV_NB] = 1;
     CK(cudaMemcpyAsync(a.scal, scal, sizeof scal, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (inc_cost)
         *inc_cost = sum[1];
     return 0;
+}
+
+extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset, int k_max,
+                             int k_vnd_max, uint64_t seed, const uint8_t *sm, const uint8_t *sr,
+                             int64_t *inc_cost)
+{
+    return rl_gvns_begin_batch(h, workers, 1, worker_offset, k_max, k_vnd_max, seed, sm, sr,
+                               inc_cost);
 }
 
 extern "C" int rl_gvns_set_strength(rl_instance *h, int64_t strength)
@@ -711,21 +831,37 @@ extern "C" int rl_gvns_set_strength(rl_instance *h, int64_t strength)
     return 0;
 }
 
+// shake -> fallback -> VND tasks -> join of one batch (round_arg < 0: at the
+// device round counter), enqueued on the handle's stream
+static int gv_launch_round(rl_instance *h, int64_t round_arg, int64_t max_rounds, int mode)
+{
+    GvnsState *gs = h->gv;
+    int rc = RL_DISPATCH(h, gv_launch_shake, h, gs, round_arg, max_rounds);
+    if (rc)
+        return rc;
+    if ((rc = RL_DISPATCH_M(h, gv_launch_vnd, h, gs)))
+        return rc;
+    k_gvns_join<<<1, 1024, 0, h->stream>>>(gs->a, mode, round_arg, max_rounds);
+    CKL();
+    return 0;
+}
+
 extern "C" int rl_gvns_round(rl_instance *h, int64_t round_index, int accept)
 {
     (void)cudaGetLastError();
     if (!h || !h->gv || round_index < 0)
         return fail(RL_EINVAL, "rl_gvns_round: call rl_gvns_begin first");
     CK(cudaSetDevice(h->device));
-    GvnsState *gs = h->gv;
-    int rc = RL_DISPATCH(h, gv_launch_shake, h, gs, round_index);
-    if (rc)
-        return rc;
-    if ((rc = RL_DISPATCH_M(h, gv_launch_vnd, h, gs)))
-        return rc;
-    k_gvns_join<<<1, 1024, 0, h->stream>>>(gs->a, accept ? 1 : 0);
-    CKL();
-    return 0;
+    return gv_launch_round(h, round_index, round_index + 1, accept ? 1 : 0);
+}
+
+extern "C" int rl_gvns_run(rl_instance *h, int64_t max_rounds)
+{
+    (void)cudaGetLastError();
+    if (!h || !h->gv || max_rounds < 0)
+        return fail(RL_EINVAL, "rl_gvns_run: call rl_gvns_begin_batch first");
+    CK(cudaSetDevice(h->device));
+    return gv_launch_round(h, -1, max_rounds, 1);
 }
 
 extern "C" int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr, int64_t *info)
@@ -752,6 +888,7 @@ extern "C" int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr
     info[3] = scal[GV_BEST_W];
     info[4] = scal[GV_ACCEPTED];
     info[5] = scal[GV_FB_COUNT];
+    info[6] = scal[GV_ROUND];
     return 0;
 }
 

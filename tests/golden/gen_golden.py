@@ -21,7 +21,7 @@ np.packbits(setup_m) || np.packbits(setup_r)):
   big.json           K=100000 T=52 and T=520 sample summaries (--big)
   rng.npz            numpy Philox/SeedSequence/choice/shuffle streams
   gvns_small.npz     shake / worker_round / gvns(max_rounds) results
-  gvns_k1000.json    K=1000 T=52 gvns(max_rounds=20, workers=2, seed=0)
+  gvns_k1000.json    K=1000 T=52 gvns(seed=0): W=2 x 20 and x 150 rounds, W=16 x 4
 """
 
 import hashlib
@@ -374,7 +374,7 @@ def gen_gvns_small():
 def gen_gvns_k1000():
     inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
     out = {}
-    for W, R in ((2, 20), (16, 4)):
+    for W, R in ((2, 20), (16, 4), (2, 150)):
         cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=W, seed=0,
                            max_rounds=R, vnd_mode="product-parallel", parallelism=8)
         t0 = time.time()
@@ -407,6 +407,9 @@ if __name__ == "__main__":
     _kernels.warm_up()
     if "--oracle-only" in sys.argv:
         gen_oracle_optimal()
+        sys.exit(0)
+    if "--gvns-k1000-only" in sys.argv:
+        gen_gvns_k1000()
         sys.exit(0)
     gen_instances()
     gen_rng()

@@ -111,6 +111,35 @@ def test_gvns_round_capped_matches_reference():
             assert np.array_equal(res.plan.setup_r, data[key + "_sr"]), key
 
 
+@pytest.mark.parametrize("batch", ["1", "2", "5", "32"])
+def test_gvns_speculative_batches_match_reference(batch, monkeypatch):
+    """Speculative batches of rounds (rl_gvns_run) reproduce the sequential
+    trajectory whatever the batch size: rounds accepted mid-batch discard the
+    rest of the batch (round-capped goldens of the live reference)."""
+    monkeypatch.setenv("RL_GVNS_BATCH", batch)
+    data, cases = _small_cases()
+    for ci in cases:
+        inst = _inst(data, ci + "_")
+        for W in (1, 3):
+            cfg = SolverConfig(t_max=1e9, k_max=3, workers=W, seed=7, max_rounds=6)
+            res = gvns(inst, cfg)
+            key = f"{ci}_gvns_W{W}"
+            assert res.cost == int(data[key + "_cost"]), key
+            assert res.rounds == int(data[key + "_rounds"])
+            assert np.array_equal(res.plan.setup_m, data[key + "_sm"]), key
+            assert np.array_equal(res.plan.setup_r, data[key + "_sr"]), key
+    with open(os.path.join(GOLDEN, "gvns_k1000.json")) as f:
+        gold = json.load(f)
+    inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+    for name, R in (("W2_R20", 20), ("W2_R150", 150)):
+        cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=2, seed=0, max_rounds=R)
+        res = gvns(inst, cfg)
+        g = gold[name]
+        assert res.cost == g["cost"] and res.rounds == R, name
+        assert res.shake_calls == g["shake_calls"]
+        assert _plan_sha(res.plan) == g["plan_sha"], name
+
+
 def test_gvns_k1000_matches_reference():
     """BASELINE config 2 (K=1000, T=52, full GVNS): round-capped runs of the
     live reference (W=2 x 20 rounds, W=16 x 4 rounds)."""
