@@ -38,6 +38,7 @@ struct GvnsArgs {
     int64_t *tailidx;                 // W x pop (only when the tail shuffle is needed)
     int64_t *tp;                      // W x tcap touched products
     int *tn, *fb, *fbslot;            // W
+    int *tasks;                       // W x tcap: compact (worker x tcap + j) VND tasks
     uint32_t *tw;                     // W x tcap x 2 x NW
     int64_t *tcost;                   // W x tcap
     PhiloxState *rng;                 // W
@@ -59,6 +60,7 @@ enum {
     GV_ERROR,
     GV_ROUND,     // rounds completed (the next batch starts here)
     GV_NB,        // rounds of the next batch (adaptive, <= B)
+    GV_NTASK,     // compact VND tasks appended by k_shake (reset by the join)
     GV_FBCOST0,   // fb_slots entries follow
 };
 
@@ -321,6 +323,11 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
             if (lane == 0) {
                 g.tn[w] = n;
                 g.fb[w] = 0;
+                // compact task list: k_gvns_vnd's warps take only real tasks
+                const int64_t b =
+                    (int64_t)atomicAdd((unsigned long long *)&g.scal[GV_NTASK], (unsigned long long)n);
+                for (int j = 0; j < n; ++j)
+                    g.tasks[b + j] = w * g.tcap + j;
             }
             return;
         }
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, in
         mbar_init(s.bar);
     __syncwarp();
     uint32_t phase = 0;
-    const int64_t n_norm = (int64_t)g.W * g.tcap;
+    const int64_t n_norm = g.scal[GV_NTASK];
     int64_t nfb = g.scal[GV_FB_COUNT];
     nfb = nfb < g.fb_slots ? nfb : g.fb_slots;
     const int64_t n_tasks = n_norm + nfb * g.K;
@@ -420,8 +427,9 @@ __global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, in
         uint8_t *plan = nullptr;
         int w = -1, j = -1, slot = -1;
         if (task < n_norm) {
-            w = (int)(task / g.tcap);
-            j = (int)(task % g.tcap);
+            const int id = g.tasks[task];
+            w = id / g.tcap;
+            j = id % g.tcap;
             if (g.fb[w] || j >= g.tn[w])
                 continue;
             k = g.tp[(int64_t)w * g.tcap + j];
@@ -507,6 +515,8 @@ __global__ void k_gvns_join(GvnsArgs g, int mode, int64_t round_arg, int64_t max
     __shared__ int s_accept, s_win;
     int64_t r0;
     const int nb = gv_batch(g, round_arg, max_rounds, r0);
+    if (threadIdx.x == 0)
+        g.scal[GV_NTASK] = 0;   // k_gvns_vnd has consumed the round's tasks
     if (nb == 0)
         return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -647,7 +657,7 @@ struct GvnsState {
     GvnsArgs a{};
     int k_vnd_max = 4;
     size_t tail_bytes = 0;
-    void *blocks[16] = {};
+    void *blocks[24] = {};
     int nblocks = 0;
 };
 
@@ -767,6 +777,7 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
             e = gv_alloc(gs, &a.tw, (size_t)slots * a.tcap * 2 * NW * 4);
         }
         if (e == cudaSuccess) e = gv_alloc(gs, &a.tcost, (size_t)slots * a.tcap * 8);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.tasks, (size_t)slots * a.tcap * sizeof(int));
         if (e == cudaSuccess) e = gv_alloc(gs, &a.rng, (size_t)slots * sizeof(PhiloxState));
         if (e == cudaSuccess) e = gv_alloc(gs, &a.fbplan, (size_t)a.fb_slots * pop);
         if (e == cudaSuccess) e = gv_alloc(gs, &a.fbdiff, (size_t)a.fb_slots * pop * 8);
@@ -804,6 +815,7 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
     scal[GV_INC_IS_F] = 0;
     scal[GV_ROUND] = 0;
     scal[GV_NB] = 1;
+    scal[GV_NTASK] = 0;
     CK(cudaMemcpyAsync(a.scal, scal, sizeof scal, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (inc_cost)
