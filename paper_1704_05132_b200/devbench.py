@@ -82,6 +82,7 @@ def other_configs(torch):
     headline; each parity-checked where a reference golden exists):
       c2_vnd  K=1000 T=52 VND to local optimum (ms; golden cost 4,484,593,955)
       c2_gvns K=1000 T=52 full GVNS, W=2, k_max=5: rounds/s over 400 rounds
+      c2_gvns_20k  the same over 20,000 rounds (speculative batches pay late)
       c4_vnd  K=10000 T=520 VND to local optimum (ms)
       c5_gvns K=1000 T=52, W=128 workers (one GPU's share of 1,024): rounds/s
     Times are device-synchronised wall clock around the C ABI calls."""
@@ -106,7 +107,8 @@ def other_configs(torch):
     inst2, ms, st = vnd_ms(1000, 52)
     out["c2_vnd"] = {"kernel_ms": ms, "cost": st["cost"], "bit_exact": st["cost"] == 4484593955,
                      "evals_reference": st["evals_reference"]}
-    for name, W, R in (("c2_gvns", 2, 400), ("c5_gvns_1gpu_share", 128, 40)):
+    for name, W, R in (("c2_gvns", 2, 400), ("c2_gvns_20k", 2, 20000),
+                       ("c5_gvns_1gpu_share", 128, 40)):
         cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=W, seed=0, max_rounds=R)
         gvns(inst2, SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=W, seed=0,
                                  max_rounds=2))
