@@ -8,8 +8,8 @@
 // is the per-product VND of its rows, a worker's
 // result is F (the per-product VND image of the incumbent, computed once)
 // with only its touched products re-descended.  So a round is:
-//   k_shake           thread per worker: draws, touched rows, feasibility
-//   k_shake_fallback  thread per worker whose 50 draws failed (gvns.py:124-137)
+//   k_shake           warp per worker: draws, touched rows, feasibility; lane 0
+//                     runs the fallback when all 50 draws failed (gvns.py:124-137)
 //   k_gvns_vnd        warp per (worker, touched product) [+ fallback plans]
 //   k_gvns_join       block: min (cost, worker) join, accept, next strength
 // with no host synchronisation; the incumbent and F stay resident.
@@ -154,6 +154,64 @@ __device__ inline bool row_feasible(const V *d, const V *r, int T, BitM bm, BitR
     return true;
 }
 
+// gvns.py:124-137: flip the positions where the incumbent differs from the
+// lot-for-lot start, in rng.shuffle order, until >= k_eff flips and the whole
+// plan is feasible; else return the start.  Run by lane 0 of the worker's
+// k_shake warp right after its 50 redraws failed (rare), with the worker's
+// RNG state after them.
+template <typename V>
+__device__ void shake_fallback(const InstView<V> &in, const GvnsArgs &g, int w,
+                               const PhiloxState &st)
+{
+    const int slot = atomicAdd((unsigned long long *)&g.scal[GV_FB_COUNT], 1ull);
+    if (slot >= g.fb_slots) {
+        atomicExch((unsigned long long *)&g.scal[GV_ERROR], 1ull);
+        return;
+    }
+    g.fbslot[w] = slot;
+    const int T = g.T;
+    const int64_t KT = g.KT, K = g.K;
+    uint8_t *plan = g.fbplan + (int64_t)slot * 2 * KT;
+    int64_t *diff = g.fbdiff + (int64_t)slot * g.pop;
+    int64_t *bad = g.fbpcost + (int64_t)slot * K;   // infeasibility flags, then costs
+    for (int64_t i = 0; i < 2 * KT; ++i)
+        plan[i] = g.inc[i];
+    int64_t n = 0;
+    for (int64_t p = 0; p < KT; ++p)
+        if (g.inc[p] != g.init[p])
+            diff[n++] = p;
+    for (int64_t p = 0; p < KT; ++p)
+        if (g.inc[KT + p] != g.init[KT + p])
+            diff[n++] = p + KT;
+    Philox rng;
+    rng.st = st;
+    rng.shuffle(diff, n);
+    const int64_t strength = gv_strength(g, w / g.Wr);
+    const int64_t k_eff = strength < g.pop ? strength : g.pop;
+    for (int64_t k = 0; k < K; ++k)
+        bad[k] = 0;   // the incumbent is feasible
+    int64_t nbad = 0;
+    bool done = false;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t p = diff[i];
+        plan[p] ^= 1;
+        const int64_t k = (p % KT) / T;
+        const uint8_t *pm = plan + k * T, *pr = plan + KT + k * T;
+        const bool f = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
+                                       [&](int q) { return pm[q] != 0; },
+                                       [&](int q) { return pr[q] != 0; });
+        nbad += (f ? 0 : 1) - bad[k];
+        bad[k] = f ? 0 : 1;
+        if (i + 1 >= k_eff && nbad == 0) {
+            done = true;
+            break;
+        }
+    }
+    if (!done)
+        for (int64_t i = 0; i < 2 * KT; ++i)
+            plan[i] = g.init[i];
+}
+
 // One warp per worker: lane 0 runs the (inherently sequential) numpy-exact
 // draw and the flips; the other lanes pull the touched products' rows
 // (incumbent bits, demand, returns) into L1 with coalesced loads first, so
@@ -164,18 +222,9 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
     extern __shared__ __align__(16) unsigned char shk[];
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (blockIdx.x == 0) {
-        // per-round counters of the kernels after this one (fallback slots,
-        // fallback plan costs, the VND task queue): reset here instead of by
-        // three memset nodes per round
-        if (threadIdx.x == 0) {
-            g.scal[GV_FB_COUNT] = 0;
-            g.scal[GV_FB_COUNT + 1] = 0;
-            *g.queue = 0;
-        }
-        for (int i = threadIdx.x; i < g.fb_slots; i += blockDim.x)
-            g.scal[GV_FBCOST0 + i] = 0;
-    }
+    // the per-round counters this kernel and the next ones use (fallback
+    // slots, fallback plan costs, task list, VND queue) were reset by the
+    // previous round's join (or rl_gvns_begin)
     if (w >= g.W)
         return;
     int64_t r0;
@@ -336,67 +385,10 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
         g.tn[w] = 0;
         g.fb[w] = 1;
         g.rng[w] = rng.st;
+        shake_fallback<V>(in, g, w, rng.st);
     }
 }
 
-// gvns.py:124-137: flip the positions where the incumbent differs from the
-// lot-for-lot start, in rng.shuffle order, until >= k_eff flips and the whole
-// plan is feasible; else return the start.  One thread per failing worker
-// (rare: all 50 independent redraws must have failed).
-template <typename V>
-__global__ void k_shake_fallback(InstView<V> in, GvnsArgs g)
-{
-    const int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= g.W || !g.fb[w])
-        return;
-    const int slot = atomicAdd((unsigned long long *)&g.scal[GV_FB_COUNT], 1ull);
-    if (slot >= g.fb_slots) {
-        atomicExch((unsigned long long *)&g.scal[GV_ERROR], 1ull);
-        return;
-    }
-    g.fbslot[w] = slot;
-    const int T = g.T;
-    const int64_t KT = g.KT, K = g.K;
-    uint8_t *plan = g.fbplan + (int64_t)slot * 2 * KT;
-    int64_t *diff = g.fbdiff + (int64_t)slot * g.pop;
-    int64_t *bad = g.fbpcost + (int64_t)slot * K;   // infeasibility flags, then costs
-    for (int64_t i = 0; i < 2 * KT; ++i)
-        plan[i] = g.inc[i];
-    int64_t n = 0;
-    for (int64_t p = 0; p < KT; ++p)
-        if (g.inc[p] != g.init[p])
-            diff[n++] = p;
-    for (int64_t p = 0; p < KT; ++p)
-        if (g.inc[KT + p] != g.init[KT + p])
-            diff[n++] = p + KT;
-    Philox rng;
-    rng.st = g.rng[w];
-    rng.shuffle(diff, n);
-    const int64_t strength = gv_strength(g, w / g.Wr);
-    const int64_t k_eff = strength < g.pop ? strength : g.pop;
-    for (int64_t k = 0; k < K; ++k)
-        bad[k] = 0;   // the incumbent is feasible
-    int64_t nbad = 0;
-    bool done = false;
-    for (int64_t i = 0; i < n; ++i) {
-        const int64_t p = diff[i];
-        plan[p] ^= 1;
-        const int64_t k = (p % KT) / T;
-        const uint8_t *pm = plan + k * T, *pr = plan + KT + k * T;
-        const bool f = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
-                                       [&](int q) { return pm[q] != 0; },
-                                       [&](int q) { return pr[q] != 0; });
-        nbad += (f ? 0 : 1) - bad[k];
-        bad[k] = f ? 0 : 1;
-        if (i + 1 >= k_eff && nbad == 0) {
-            done = true;
-            break;
-        }
-    }
-    if (!done)
-        for (int64_t i = 0; i < 2 * KT; ++i)
-            plan[i] = g.init[i];
-}
 
 // VND of every (worker, touched product) task and of every product of the
 // fallback plans; warps pull tasks from a queue.
@@ -515,8 +507,14 @@ __global__ void k_gvns_join(GvnsArgs g, int mode, int64_t round_arg, int64_t max
     __shared__ int s_accept, s_win;
     int64_t r0;
     const int nb = gv_batch(g, round_arg, max_rounds, r0);
-    if (threadIdx.x == 0)
-        g.scal[GV_NTASK] = 0;   // k_gvns_vnd has consumed the round's tasks
+    if (threadIdx.x == 0) {
+        // k_gvns_vnd has consumed the round's tasks: per-round counters for
+        // the next round (fallback plan costs are reset after the join reads
+        // them)
+        g.scal[GV_NTASK] = 0;
+        g.scal[GV_FB_COUNT] = 0;
+        *g.queue = 0;
+    }
     if (nb == 0)
         return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -602,6 +600,8 @@ __global__ void k_gvns_join(GvnsArgs g, int mode, int64_t round_arg, int64_t max
         s_win = win;
     }
     __syncthreads();
+    for (int i = tid; i < g.fb_slots; i += blockDim.x)
+        g.scal[GV_FBCOST0 + i] = 0;   // read (gv_worker_cost) before the barrier above
     const int win = s_win;
     if (!s_accept)
         return;
@@ -706,8 +706,6 @@ static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round_arg,
     const int W = gs->a.W;
     k_shake<V><<<(W + 3) / 4, 128, 4 * (size_t)gs->a.shake_bytes, h->stream>>>(
         view<V>(h), gs->a, round_arg, max_rounds);
-    CKL();
-    k_shake_fallback<V><<<(W + 63) / 64, 64, 0, h->stream>>>(view<V>(h), gs->a);
     CKL();
     return 0;
 }
@@ -816,6 +814,8 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
     scal[GV_ROUND] = 0;
     scal[GV_NB] = 1;
     scal[GV_NTASK] = 0;
+    CK(cudaMemsetAsync(a.scal, 0, (GV_FBCOST0 + a.fb_slots) * sizeof(int64_t), h->stream));
+    CK(cudaMemsetAsync(a.queue, 0, 16, h->stream));
     CK(cudaMemcpyAsync(a.scal, scal, sizeof scal, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (inc_cost)

@@ -180,3 +180,22 @@ def test_sharded_replicas_device_backend_single_rank():
         assert _plan_sha(res.plan) == g["plan_sha"]
     finally:
         dist.destroy_process_group()
+
+
+def test_gvns_time_budget_follows_the_round_capped_trajectory():
+    """A wall-clock-limited run (gvns.py:199-202: clock checked between
+    rounds; here between in-flight speculative batches) stops near t_max and
+    its result is the round-capped run with the same round count: the
+    speculative batches never change the trajectory."""
+    import time
+    from paper_1704_05132_b200 import evaluate
+    inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+    t0 = time.monotonic()
+    res = gvns(inst, SolverConfig(t_max=0.3, k_max=5, k_vnd_max=4, workers=2, seed=0))
+    assert time.monotonic() - t0 < 5.0
+    assert res.rounds > 0 and res.shake_calls == 2 * res.rounds
+    assert evaluate(inst, res.plan) == res.cost
+    capped = gvns(inst, SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=2, seed=0,
+                                     max_rounds=res.rounds))
+    assert capped.rounds == res.rounds and capped.cost == res.cost
+    assert _plan_sha(capped.plan) == _plan_sha(res.plan)
