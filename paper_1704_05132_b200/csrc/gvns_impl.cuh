@@ -659,12 +659,19 @@ struct GvnsState {
     size_t tail_bytes = 0;
     void *blocks[24] = {};
     int nblocks = 0;
+    // rl_gvns_run's batch (shake, VND tasks, join) as one CUDA graph: its
+    // arguments are fixed between rl_gvns_begin calls except max_rounds
+    cudaGraphExec_t graph = nullptr;
+    int64_t graph_max = -1;
+    int runs = 0;
 };
 
 static void gvns_free(GvnsState *gs)
 {
     if (!gs)
         return;
+    if (gs->graph)
+        cudaGraphExecDestroy(gs->graph);
     for (int i = 0; i < gs->nblocks; ++i)
         if (gs->blocks[i])
             cudaFree(gs->blocks[i]);
@@ -790,6 +797,11 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
     GvnsArgs &a = gs->a;
     a.seed = seed;
     a.w0 = worker_offset;
+    if (gs->graph) {   // captured with the previous arguments
+        cudaGraphExecDestroy(gs->graph);
+        gs->graph = nullptr;
+    }
+    gs->runs = 0;
     gs->k_vnd_max = k_vnd_max;
     // incumbent, lot-for-lot start, and F = per-product VND image of the incumbent
     CK(cudaMemcpyAsync(a.inc, sm, KT, cudaMemcpyHostToDevice, h->stream));
@@ -873,7 +885,41 @@ extern "C" int rl_gvns_run(rl_instance *h, int64_t max_rounds)
     if (!h || !h->gv || max_rounds < 0)
         return fail(RL_EINVAL, "rl_gvns_run: call rl_gvns_begin_batch first");
     CK(cudaSetDevice(h->device));
-    return gv_launch_round(h, -1, max_rounds, 1);
+    GvnsState *gs = h->gv;
+    if (gs->graph && gs->graph_max == max_rounds) {
+        CK(cudaGraphLaunch(gs->graph, h->stream));
+        h->launches += 3;
+        return 0;
+    }
+    if (gs->runs++ == 0)   // first batch launched plainly (sets kernel attributes)
+        return gv_launch_round(h, -1, max_rounds, 1);
+    if (gs->graph) {
+        cudaGraphExecDestroy(gs->graph);
+        gs->graph = nullptr;
+    }
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = h->launches;
+    const int rc = gv_launch_round(h, -1, max_rounds, 1);
+    const cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+    h->launches = l0;
+    if (rc) {
+        if (e == cudaSuccess)
+            cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (e != cudaSuccess)
+        return fail(RL_ECUDA, "rl_gvns_run: capture: %s", cudaGetErrorString(e));
+    const cudaError_t ei = cudaGraphInstantiate(&gs->graph, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        gs->graph = nullptr;
+        return fail(RL_ECUDA, "rl_gvns_run: graph: %s", cudaGetErrorString(ei));
+    }
+    gs->graph_max = max_rounds;
+    CK(cudaGraphLaunch(gs->graph, h->stream));
+    h->launches += 3;
+    return 0;
 }
 
 extern "C" int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr, int64_t *info)
