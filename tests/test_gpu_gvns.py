@@ -199,3 +199,18 @@ def test_gvns_time_budget_follows_the_round_capped_trajectory():
                                      max_rounds=res.rounds))
     assert capped.rounds == res.rounds and capped.cost == res.cost
     assert _plan_sha(capped.plan) == _plan_sha(res.plan)
+
+
+def test_gvns_graph_replay_across_runs_on_one_handle():
+    """rl_gvns_run's captured graph is rebuilt when the run's arguments
+    change: runs with another seed, another round cap and the golden's again
+    on the same cached device handle reproduce the golden."""
+    with open(os.path.join(GOLDEN, "gvns_k1000.json")) as f:
+        g = json.load(f)["W2_R20"]
+    inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+    base = dict(t_max=1e9, k_max=5, k_vnd_max=4, workers=2)
+    other = gvns(inst, SolverConfig(seed=3, max_rounds=20, **base))
+    assert other.rounds == 20
+    gvns(inst, SolverConfig(seed=0, max_rounds=7, **base))
+    res = gvns(inst, SolverConfig(seed=0, max_rounds=20, **base))
+    assert res.cost == g["cost"] and _plan_sha(res.plan) == g["plan_sha"]
