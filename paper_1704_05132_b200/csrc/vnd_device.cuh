@@ -356,35 +356,26 @@ struct MaskSmem {
 struct PatchedSmem {
     MaskSmem base;
     int a, b, ta, tb;
-    // first setup >= x (T if none) and its kind
-    // (x <= T: nx[T] = T is the end entry)
+    // First setup >= x (T if none) and its kind, for the queries of a delta
+    // walk (walk_moves): x = 0 when the base plan has no setup before a, else
+    // x > prev(a).  The base plan then has no setup in [x, a), and none
+    // strictly between a and b (b = a, or b = a + 1 for N3 shifts), so for
+    // x <= b the answer is a (if set and x <= a), else b (if set), else the
+    // first base setup after b; past b it is the table entry.  x <= T
+    // (nx[T] = T is the end entry).
     __device__ int next_t(int x, int &ty) const
     {
-        const int T = base.T;
-        int e = base.nx[x];
+        const int e = base.nx[x > b ? x : b + 1];
         int t = e & kPeriodMask;
         ty = e >> kTypeShift;
-        // past the move (x > b >= a) the rows are the base rows; most walk
-        // steps take only the lookup above
         if (x <= b) {
-            // base setups the move clears (at most a and b) are skipped
-#pragma unroll 1
-            while (t < T && (t == a || t == b)) {
-                const int pt = t == a ? ta : tb;
-                if (pt) {
-                    ty = pt;
-                    break;
-                }
-                e = base.nx[t + 1];
-                t = e & kPeriodMask;
-                ty = e >> kTypeShift;
-            }
-            if (x <= a && a < t && ta) {
-                t = a;
-                ty = ta;
-            } else if (b < t && tb) {
+            if (tb) {
                 t = b;
                 ty = tb;
+            }
+            if (x <= a && ta) {
+                t = a;
+                ty = ta;
             }
         }
         return t;
