@@ -398,15 +398,19 @@ __global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, in
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int T = in.T, NW = g.NW;
+    const int64_t n_norm = g.scal[GV_NTASK];
+    int64_t nfb = g.scal[GV_FB_COUNT];
+    nfb = nfb < g.fb_slots ? nfb : g.fb_slots;
+    const int64_t n_tasks = n_norm + nfb * g.K;
+    // warps beyond the round's task count leave before touching the queue
+    // (the grid is sized for the worst case: every slot's tasks + fallbacks)
+    if ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp >= n_tasks)
+        return;
     Slot<V, C> s = carve<V, C>(smem + warp * slot_bytes<V, C>(T), T);
     if (lane == 0)
         mbar_init(s.bar);
     __syncwarp();
     uint32_t phase = 0;
-    const int64_t n_norm = g.scal[GV_NTASK];
-    int64_t nfb = g.scal[GV_FB_COUNT];
-    nfb = nfb < g.fb_slots ? nfb : g.fb_slots;
-    const int64_t n_tasks = n_norm + nfb * g.K;
     for (;;) {
         int64_t task = 0;
         if (lane == 0)
