@@ -365,6 +365,7 @@ struct PatchedSmem {
     // (nx[T] = T is the end entry).
     __device__ int next_t(int x, int &ty) const
     {
+        RL_ASSERT(x > b || (base.nx[x] & kPeriodMask) >= a);   // no base setup in [x, a)
         const int e = base.nx[x > b ? x : b + 1];
         int t = e & kPeriodMask;
         ty = e >> kTypeShift;
