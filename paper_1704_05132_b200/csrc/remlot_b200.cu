@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int T = in.T;
     const Slot<V, C> s = carve<V, C>(smem, T);
-    const MaskSmem mk{s.bm, s.br, s.nx, T};
+    const MaskSmem mk{s.bm, s.br, s.bs, s.nx, T};
     if (threadIdx.x == 0) {
         mbar_init(s.bar);
         sh_k = o.k_lo + atomicAdd(o.queue, 1);

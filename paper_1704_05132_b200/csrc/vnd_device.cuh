@@ -12,7 +12,7 @@
 //               (C) and cumulative remanufactured quantity entering u (V)
 //   slk[T]      remanufacturing slack CR[u] - xin[u] - seg(u) at sR setups (V)
 //   lm[18]      T <= 63: masks of sR setups with slack < 2^j (j < 16), all sR, slack < 0
-//   bm[NW],br[NW]  setup bit rows (uint32 words; used when T > 64)
+//   bm[NW],br[NW],bs[NW]  setup bit rows and their union (uint32 words; T > 63)
 //   mv[2T+2]    compacted move slots of the current neighborhood (uint16)
 //
 // For T <= 63 the setup rows live in registers instead (two warp-uniform
@@ -133,7 +133,7 @@ struct Slot {
     DR<V> *dr;
     XCStore<V, C> xc;
     uint16_t *nx;       // T > 63: next setup >= t of the base plan and its kind
-    uint32_t *bm, *br;
+    uint32_t *bm, *br, *bs;
     uint16_t *mv;
     uint64_t *lm;
     uint64_t *bar;
@@ -162,7 +162,7 @@ __host__ __device__ inline size_t slot_bytes(int T)
     b += align16(XCStore<V, C>::bytes(T + 1));         // xc (+ the end entry xc[T])
     b += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));   // slk (register-mask path only)
     b += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));   // nx
-    b += align16(2 * (size_t)NW * sizeof(uint32_t));
+    b += align16(3 * (size_t)NW * sizeof(uint32_t));
     b += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
     b += align16((kSlackLevels + 2) * 8);        // lm
     b += 16;                                     // mbarrier
@@ -184,7 +184,8 @@ __device__ inline Slot<V, C> carve(unsigned char *base, int T)
     s.slk = (V *)p;   p += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));
     s.nx = (uint16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(uint16_t));
     s.bm = (uint32_t *)p;
-    s.br = s.bm + NW; p += align16(2 * (size_t)NW * sizeof(uint32_t));
+    s.br = s.bm + NW;
+    s.bs = s.br + NW; p += align16(3 * (size_t)NW * sizeof(uint32_t));
     s.mv = (uint16_t *)p; p += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
     s.lm = (uint64_t *)p; p += align16((kSlackLevels + 2) * 8);
     s.bar = (uint64_t *)p;
@@ -263,12 +264,12 @@ constexpr int kTypeShift = 14;
 constexpr int kPeriodMask = (1 << kTypeShift) - 1;   // T <= 16000 < 2^14
 
 struct MaskSmem {
-    uint32_t *bm, *br;
+    uint32_t *bm, *br, *bs;   // bs = bm | br (one load per setup query)
     uint16_t *nx;
     int T;
     __device__ bool m(int t) const { return wbit(bm, t); }
     __device__ bool r(int t) const { return wbit(br, t); }
-    __device__ bool setup(int t) const { return wbit(bm, t) | wbit(br, t); }
+    __device__ bool setup(int t) const { return wbit(bs, t); }
     // smallest setup period >= x (T if none); needs fresh tables
     __device__ int next(int x) const
     {
@@ -284,10 +285,10 @@ struct MaskSmem {
         if (x <= 0)
             return -1;
         int w = (x - 1) >> 5;
-        uint32_t bits = (bm[w] | br[w]) & (0xffffffffu >> (31 - ((x - 1) & 31)));
+        uint32_t bits = bs[w] & (0xffffffffu >> (31 - ((x - 1) & 31)));
         while (!bits && w > 0) {
             --w;
-            bits = bm[w] | br[w];
+            bits = bs[w];
         }
         return bits ? (w << 5) + 31 - __clz(bits) : -1;
     }
@@ -295,8 +296,11 @@ struct MaskSmem {
     {
         if (lane == 0) {
             const uint32_t b = 1u << (t & 31);
-            bm[t >> 5] = mv ? (bm[t >> 5] | b) : (bm[t >> 5] & ~b);
-            br[t >> 5] = rv ? (br[t >> 5] | b) : (br[t >> 5] & ~b);
+            const uint32_t wm = mv ? (bm[t >> 5] | b) : (bm[t >> 5] & ~b);
+            const uint32_t wr = rv ? (br[t >> 5] | b) : (br[t >> 5] & ~b);
+            bm[t >> 5] = wm;
+            br[t >> 5] = wr;
+            bs[t >> 5] = wm | wr;
         }
     }
     __device__ void sync() const { __syncwarp(); }
@@ -311,10 +315,10 @@ struct MaskSmem {
         if (lo < hi) {
             int w = lo >> 5;
             const int wl = (hi - 1) >> 5;
-            uint32_t bits = (bm[w] | br[w]) & (0xffffffffu << (lo & 31));
+            uint32_t bits = bs[w] & (0xffffffffu << (lo & 31));
             while (!bits && w < wl) {
                 ++w;
-                bits = bm[w] | br[w];
+                bits = bs[w];
             }
             const int f = bits ? (w << 5) + __ffs(bits) - 1 : T;
             first = f < hi ? f : T;
@@ -473,10 +477,11 @@ __device__ inline MaskSmem load_rows(const Slot<V, C> &s, MaskSmem, const uint8_
         if (lane == 0) {
             s.bm[base >> 5] = wm;
             s.br[base >> 5] = wr;
+            s.bs[base >> 5] = wm | wr;
         }
     }
     __syncwarp();
-    return MaskSmem{s.bm, s.br, s.nx, T};
+    return MaskSmem{s.bm, s.br, s.bs, s.nx, T};
 }
 
 template <typename V, typename C>
