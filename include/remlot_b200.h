@@ -16,7 +16,11 @@
  *   - caller-allocated outputs; return 0 on success, negative on error
  *     (RL_E*), message in rl_last_error() (thread-local);
  *   - a handle is bound to the CUDA device that was current at creation;
- *     calls on one handle must not overlap (one handle per thread/stream).
+ *   - thread safety: every entry point taking a handle holds the handle's
+ *     mutex for the call (single calls may come from any thread); no entry
+ *     point synchronises the whole device.  Multi-call sequences over state
+ *     kept on the handle (rl_vnd_device + rl_vnd_collect, the rl_gvns_*
+ *     session) need one handle per concurrent user.
  */
 #ifndef REMLOT_B200_H
 #define REMLOT_B200_H
@@ -63,7 +67,9 @@ int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uint8_t *sr);
  * tests).  Bit 0: reserved (was two products per warp; removed, RL_EINVAL).
  * Bit 1: T > 63 never uses one CTA per product (by default
  * a CTA per product is used when K <= 2 x SMs, a warp per product above).
- * Bits 2/3: T <= 63 slack skip always / never (default: per launch). */
+ * Bits 2/3: T <= 63 slack skip always / never (default: per launch).
+ * Bit 4: int64 values and int64 costs whatever the range proof allows (the
+ * general path; the narrow exact widths are the default). */
 int rl_instance_set_variant(rl_instance *h, int variant);
 /* info[0..5] = K, T, bytes per period value (4|8), bytes per cost (4|8),
  * SM count, warps per CTA of the resident VND kernel. */

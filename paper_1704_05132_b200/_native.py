@@ -5,8 +5,10 @@ device is visible, every call raises.  The library is built in-tree by
 ``paper_1704_05132_b200.build`` (nvcc, sm_100a) into ``_lib/``.
 """
 
+import contextlib
 import ctypes
 import os
+import threading
 
 import numpy as np
 
@@ -154,6 +156,11 @@ class DeviceInstance:
 
     def _bind(self, h):
         self.h = h
+        self.session_lock = threading.Lock()
+        self._refresh_info()
+
+    def _refresh_info(self):
+        h = self.h
         info = np.zeros(6, np.int64)
         check(load().rl_instance_info(h, ptr(info)), "rl_instance_info")
         self.K = int(info[0])
@@ -170,8 +177,10 @@ class DeviceInstance:
     def set_variant(self, variant):
         """Kernel variant bits (identical results; A/B and tests): 2 = warp
         (not CTA) per product for T > 63; 4 / 8 = slack skip always / never
-        for T <= 63; 0 = default (chosen per launch)."""
+        for T <= 63; 16 = int64 values and costs (the general path);
+        0 = default (chosen per launch)."""
         check(load().rl_instance_set_variant(self.h, int(variant)), "rl_instance_set_variant")
+        self._refresh_info()
 
     @property
     def launches(self):
@@ -181,6 +190,7 @@ class DeviceInstance:
         arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in inst.arrays()]
         check(load().rl_instance_update(self.h, *[ptr(a) for a in arrays]),
               "rl_instance_update")
+        self._refresh_info()
 
     def product_costs(self, sm, sr, lo=0, hi=None):
         hi = self.K if hi is None else hi
@@ -365,13 +375,61 @@ def rng_probe(seed, round_index, worker, pop, size, shuffle_n):
             out[-1:].view(np.uint64))
 
 
-def device_instance(inst):
-    """The cached DeviceInstance of ``inst`` (uploaded once per Instance)."""
-    dev = getattr(inst, "_device", None)
-    if dev is None:
-        dev = DeviceInstance(inst)
+class _DeviceCache:
+    """An Instance's device copies: the primary handle (single-call entry
+    points; the C ABI serialises calls on one handle) and spare handles for
+    concurrent multi-call sessions (a GVNS run keeps its state on the handle
+    between calls).  ``snapshot`` is the host data the handles hold: the
+    reference re-reads the arrays on every call, so an in-place edit of the
+    Instance must invalidate the copies (compared at each lookup)."""
+
+    def __init__(self, inst):
+        self.snapshot = tuple(np.array(a, copy=True) for a in inst.arrays())
+        self.primary = DeviceInstance(inst)
+        self.lock = threading.Lock()
+        self.handles = [self.primary]
+
+    def matches(self, inst):
+        return all(a.shape == b.shape and np.array_equal(a, b)
+                   for a, b in zip(inst.arrays(), self.snapshot))
+
+
+def _cache(inst):
+    cache = getattr(inst, "_device", None)
+    if cache is None or not cache.matches(inst):
+        cache = _DeviceCache(inst)
         try:
-            inst._device = dev
+            inst._device = cache
         except AttributeError:
             pass
-    return dev
+    return cache
+
+
+def device_instance(inst):
+    """The cached DeviceInstance of ``inst`` (uploaded once per Instance
+    content; re-uploaded after the arrays change)."""
+    return _cache(inst).primary
+
+
+@contextlib.contextmanager
+def session(inst):
+    """A handle of ``inst`` owned by the caller for a multi-call sequence
+    (device GVNS): the first idle cached handle, else a new one.  Concurrent
+    gvns()/worker_round() calls on one Instance (reference bench.py:196-198,
+    SPEC.md:351) each get their own device state."""
+    cache = _cache(inst)
+    dev = None
+    with cache.lock:
+        for d in cache.handles:
+            if d.session_lock.acquire(blocking=False):
+                dev = d
+                break
+    if dev is None:
+        dev = DeviceInstance(inst)
+        dev.session_lock.acquire()
+        with cache.lock:
+            cache.handles.append(dev)
+    try:
+        yield dev
+    finally:
+        dev.session_lock.release()

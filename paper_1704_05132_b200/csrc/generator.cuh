@@ -398,6 +398,7 @@ extern "C" int rl_instance_download(rl_instance *h, int64_t *demand, int64_t *re
                                     int64_t *setup_m, int64_t *setup_r, int64_t *hold_m,
                                     int64_t *hold_r, int64_t *unit_m, int64_t *unit_r)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !demand || !returns || !setup_m || !setup_r || !hold_m || !hold_r || !unit_m ||
         !unit_r)

@@ -61,6 +61,7 @@ enum {
     GV_ROUND,     // rounds completed (the next batch starts here)
     GV_NB,        // rounds of the next batch (adaptive, <= B)
     GV_NTASK,     // compact VND tasks appended by k_shake (reset by the join)
+    GV_FB_TRUNC,  // B - (first batch round whose fallback found no slot), 0 = none
     GV_FBCOST0,   // fb_slots entries follow
 };
 
@@ -156,60 +157,84 @@ __device__ inline bool row_feasible(const V *d, const V *r, int T, BitM bm, BitR
 
 // gvns.py:124-137: flip the positions where the incumbent differs from the
 // lot-for-lot start, in rng.shuffle order, until >= k_eff flips and the whole
-// plan is feasible; else return the start.  Run by lane 0 of the worker's
-// k_shake warp right after its 50 redraws failed (rare), with the worker's
-// RNG state after them.
+// plan is feasible; else return the start.  Run by the worker's whole k_shake
+// warp right after its 50 redraws failed (rare), with the worker's RNG state
+// after them (g.rng[w]): the warp copies the plan and compacts the differing
+// positions (ballot prefix sums keep them ascending, m rows then r rows like
+// the reference), lane 0 runs the shuffle and the flip/feasibility walk.
 template <typename V>
-__device__ void shake_fallback(const InstView<V> &in, const GvnsArgs &g, int w,
-                               const PhiloxState &st)
+__device__ void shake_fallback(const InstView<V> &in, const GvnsArgs &g, int w, int lane)
 {
-    const int slot = atomicAdd((unsigned long long *)&g.scal[GV_FB_COUNT], 1ull);
-    if (slot >= g.fb_slots) {
-        atomicExch((unsigned long long *)&g.scal[GV_ERROR], 1ull);
-        return;
-    }
-    g.fbslot[w] = slot;
-    const int T = g.T;
-    const int64_t KT = g.KT, K = g.K;
-    uint8_t *plan = g.fbplan + (int64_t)slot * 2 * KT;
-    int64_t *diff = g.fbdiff + (int64_t)slot * g.pop;
-    int64_t *bad = g.fbpcost + (int64_t)slot * K;   // infeasibility flags, then costs
-    for (int64_t i = 0; i < 2 * KT; ++i)
-        plan[i] = g.inc[i];
-    int64_t n = 0;
-    for (int64_t p = 0; p < KT; ++p)
-        if (g.inc[p] != g.init[p])
-            diff[n++] = p;
-    for (int64_t p = 0; p < KT; ++p)
-        if (g.inc[KT + p] != g.init[KT + p])
-            diff[n++] = p + KT;
-    Philox rng;
-    rng.st = st;
-    rng.shuffle(diff, n);
-    const int64_t strength = gv_strength(g, w / g.Wr);
-    const int64_t k_eff = strength < g.pop ? strength : g.pop;
-    for (int64_t k = 0; k < K; ++k)
-        bad[k] = 0;   // the incumbent is feasible
-    int64_t nbad = 0;
-    bool done = false;
-    for (int64_t i = 0; i < n; ++i) {
-        const int64_t p = diff[i];
-        plan[p] ^= 1;
-        const int64_t k = (p % KT) / T;
-        const uint8_t *pm = plan + k * T, *pr = plan + KT + k * T;
-        const bool f = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
-                                       [&](int q) { return pm[q] != 0; },
-                                       [&](int q) { return pr[q] != 0; });
-        nbad += (f ? 0 : 1) - bad[k];
-        bad[k] = f ? 0 : 1;
-        if (i + 1 >= k_eff && nbad == 0) {
-            done = true;
-            break;
+    int slot = 0;
+    if (lane == 0) {
+        slot = (int)atomicAdd((unsigned long long *)&g.scal[GV_FB_COUNT], 1ull);
+        if (slot >= g.fb_slots) {
+            // slots ran out (speculative rounds of a batch share them): the
+            // join truncates the batch before this worker's round, which is
+            // re-run later with the slots to itself; fbslot = fb_slots is
+            // never read
+            g.fbslot[w] = g.fb_slots;
+            atomicMax((unsigned long long *)&g.scal[GV_FB_TRUNC],
+                      (unsigned long long)(g.B - w / g.Wr));
+        } else {
+            g.fbslot[w] = slot;
         }
     }
+    slot = __shfl_sync(FULL, slot, 0);
+    if (slot >= g.fb_slots)
+        return;
+    const int T = g.T;
+    const int64_t KT = g.KT, K = g.K, KT2 = 2 * KT;
+    uint8_t *plan = g.fbplan + (int64_t)slot * KT2;
+    int64_t *diff = g.fbdiff + (int64_t)slot * g.pop;
+    int64_t *bad = g.fbpcost + (int64_t)slot * K;   // infeasibility flags, then costs
+    int64_t n = 0;
+    for (int64_t base = 0; base < KT2; base += 32) {
+        const int64_t p = base + lane;
+        uint8_t v = 0;
+        bool d = false;
+        if (p < KT2) {
+            v = g.inc[p];
+            plan[p] = v;
+            d = v != g.init[p];
+        }
+        const uint32_t bal = __ballot_sync(FULL, d);
+        if (d)
+            diff[n + __popc(bal & ((1u << lane) - 1u))] = p;
+        n += __popc(bal);
+    }
+    for (int64_t k = lane; k < K; k += 32)
+        bad[k] = 0;   // the incumbent is feasible
+    __syncwarp();
+    int done = 0;
+    if (lane == 0) {
+        Philox rng;
+        rng.st = g.rng[w];
+        rng.shuffle(diff, n);
+        const int64_t strength = gv_strength(g, w / g.Wr);
+        const int64_t k_eff = strength < g.pop ? strength : g.pop;
+        int64_t nbad = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t p = diff[i];
+            plan[p] ^= 1;
+            const int64_t k = (p % KT) / T;
+            const uint8_t *pm = plan + k * T, *pr = plan + KT + k * T;
+            const bool f = row_feasible<V>(in.dem + k * T, in.ret + k * T, T,
+                                           [&](int q) { return pm[q] != 0; },
+                                           [&](int q) { return pr[q] != 0; });
+            nbad += (f ? 0 : 1) - bad[k];
+            bad[k] = f ? 0 : 1;
+            if (i + 1 >= k_eff && nbad == 0) {
+                done = 1;
+                break;
+            }
+        }
+    }
+    done = __shfl_sync(FULL, done, 0);
     if (!done)
-        for (int64_t i = 0; i < 2 * KT; ++i)
+        for (int64_t i = lane; i < KT2; i += 32)
             plan[i] = g.init[i];
+    __syncwarp();
 }
 
 // One warp per worker: lane 0 runs the (inherently sequential) numpy-exact
@@ -385,8 +410,9 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
         g.tn[w] = 0;
         g.fb[w] = 1;
         g.rng[w] = rng.st;
-        shake_fallback<V>(in, g, w, rng.st);
     }
+    __syncwarp();
+    shake_fallback<V>(in, g, w, lane);
 }
 
 
@@ -508,19 +534,39 @@ __global__ void k_gvns_join(GvnsArgs g, int mode, int64_t round_arg, int64_t max
 {
     __shared__ long long s_cost[32];
     __shared__ int s_w[32];
-    __shared__ int s_accept, s_win;
+    __shared__ int s_accept, s_win, s_nb;
     int64_t r0;
-    const int nb = gv_batch(g, round_arg, max_rounds, r0);
+    const int nb_all = gv_batch(g, round_arg, max_rounds, r0);
     if (threadIdx.x == 0) {
+        // rounds from the first one with a fallback that found no slot on
+        // are discarded (re-run by the next batch, like rounds after an
+        // acceptance)
+        const int64_t tr = g.scal[GV_FB_TRUNC];
+        int nb = nb_all;
+        if (tr > 0 && g.B - tr < nb)
+            nb = (int)(g.B - tr);
+        if (nb == 0 && nb_all > 0) {
+            if (nb_all == 1)   // one round's fallbacks alone exceed the slots
+                g.scal[GV_ERROR] = 1;
+            else if (round_arg < 0)
+                g.scal[GV_NB] = 1;   // re-run the first round alone
+        }
+        s_nb = nb;
         // k_gvns_vnd has consumed the round's tasks: per-round counters for
         // the next round (fallback plan costs are reset after the join reads
         // them)
         g.scal[GV_NTASK] = 0;
         g.scal[GV_FB_COUNT] = 0;
+        g.scal[GV_FB_TRUNC] = 0;
         *g.queue = 0;
     }
-    if (nb == 0)
+    __syncthreads();
+    const int nb = s_nb;
+    if (nb == 0) {
+        for (int i = threadIdx.x; i < g.fb_slots; i += blockDim.x)
+            g.scal[GV_FBCOST0 + i] = 0;
         return;
+    }
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int nwarps = (int)(blockDim.x >> 5);
     if (g.B == 1) {
@@ -668,6 +714,7 @@ struct GvnsState {
     cudaGraphExec_t graph = nullptr;
     int64_t graph_max = -1;
     int runs = 0;
+    int vbytes = 0;   // value width the shake scratch was sized for
 };
 
 static void gvns_free(GvnsState *gs)
@@ -725,6 +772,7 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
                                    int k_max, int k_vnd_max, uint64_t seed, const uint8_t *sm,
                                    const uint8_t *sr, int64_t *inc_cost)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !sm || !sr || workers < 1 || batch < 1 || batch > 32 ||
         (int64_t)workers * batch > (1 << 20) || worker_offset < 0 || k_max < 1 ||
@@ -738,10 +786,12 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
     const int T = h->T, NW = (T + 31) / 32;
     const int64_t keff_max = k_max < pop ? k_max : pop;
     GvnsState *gs = h->gv;
-    const bool reuse = gs && gs->a.Wr == workers && gs->a.B == batch && gs->a.k_max == k_max;
+    const bool reuse = gs && gs->a.Wr == workers && gs->a.B == batch && gs->a.k_max == k_max &&
+                       gs->vbytes == h->vbytes;
     if (!reuse) {
         gvns_free(gs);
         h->gv = gs = new GvnsState();
+        gs->vbytes = h->vbytes;
         GvnsArgs &a = gs->a;
         a.K = K;
         a.KT = KT;
@@ -761,11 +811,20 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
                              align16((size_t)a.tcap * 2 * (T + 1) * h->vbytes);
             a.shake_bytes = 4 * b <= 48 * 1024 ? (int)b : 0;
         }
+        // fallback plans: enough slots for one round's workers (speculative
+        // rounds past a slot overflow are truncated by the join) within a
+        // 512 MB budget
         const double per_slot = (double)pop * (1 + 8) + 8.0 * K;
         int fbs = (int)(512.0 * (1 << 20) / per_slot);
         fbs = fbs < 1 ? 1 : fbs;
         fbs = fbs > slots ? slots : fbs;
-        a.fb_slots = fbs > 64 && slots > 64 ? 64 : fbs;
+        const int fcap = workers > 64 ? workers : 64;
+        a.fb_slots = fbs > fcap ? fcap : fbs;
+        if (const char *env = getenv("RL_GVNS_FB_SLOTS")) {   // test hook: fewer slots
+            const int n = atoi(env);
+            if (n >= 1 && n < a.fb_slots)
+                a.fb_slots = n;
+        }
         cudaError_t e = gv_alloc(gs, &a.inc, 4 * (size_t)pop);
         if (e == cudaSuccess) {
             a.F = a.inc + pop;
@@ -843,12 +902,14 @@ extern "C" int rl_gvns_begin(rl_instance *h, int workers, int64_t worker_offset,
                              int k_vnd_max, uint64_t seed, const uint8_t *sm, const uint8_t *sr,
                              int64_t *inc_cost)
 {
+    RL_GUARD(h);
     return rl_gvns_begin_batch(h, workers, 1, worker_offset, k_max, k_vnd_max, seed, sm, sr,
                                inc_cost);
 }
 
 extern "C" int rl_gvns_set_strength(rl_instance *h, int64_t strength)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !h->gv || strength < 1)
         return fail(RL_EINVAL, "rl_gvns_set_strength: bad arguments");
@@ -876,6 +937,7 @@ static int gv_launch_round(rl_instance *h, int64_t round_arg, int64_t max_rounds
 
 extern "C" int rl_gvns_round(rl_instance *h, int64_t round_index, int accept)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !h->gv || round_index < 0)
         return fail(RL_EINVAL, "rl_gvns_round: call rl_gvns_begin first");
@@ -885,6 +947,7 @@ extern "C" int rl_gvns_round(rl_instance *h, int64_t round_index, int accept)
 
 extern "C" int rl_gvns_run(rl_instance *h, int64_t max_rounds)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !h->gv || max_rounds < 0)
         return fail(RL_EINVAL, "rl_gvns_run: call rl_gvns_begin_batch first");
@@ -928,6 +991,7 @@ extern "C" int rl_gvns_run(rl_instance *h, int64_t max_rounds)
 
 extern "C" int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr, int64_t *info)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !h->gv || !info)
         return fail(RL_EINVAL, "rl_gvns_state: bad arguments");
@@ -962,6 +1026,7 @@ extern "C" int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr
 // rl_gvns_import makes a plan (a VND fixpoint) the incumbent and its own F.
 extern "C" int rl_gvns_candidate(rl_instance *h, uint8_t *d_plan, int64_t *best)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !h->gv || !best)
         return fail(RL_EINVAL, "rl_gvns_candidate: bad arguments");
@@ -982,6 +1047,7 @@ extern "C" int rl_gvns_candidate(rl_instance *h, uint8_t *d_plan, int64_t *best)
 
 extern "C" int rl_gvns_import(rl_instance *h, const uint8_t *d_plan, int64_t cost)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !h->gv || !d_plan)
         return fail(RL_EINVAL, "rl_gvns_import: bad arguments");

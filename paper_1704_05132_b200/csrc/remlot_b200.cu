@@ -13,8 +13,10 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -48,6 +50,14 @@ static int fail(int code, const char *fmt, ...)
             return fail(RL_ECUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), \
                         __FILE__, __LINE__);                                           \
     } while (0)
+
+// Calls on one handle are serialised by its recursive mutex (the reference's
+// kernels are nogil and reentrant, _kernels.py:3-4; bench.py:196-198 runs
+// solve_scheme from several threads on one Instance).  Recursive: entry
+// points call each other (rl_vnd -> rl_vnd_device -> ...).
+#define RL_GUARD(h) \
+    std::unique_lock<std::recursive_mutex> rl_guard_ = (h) ? std::unique_lock<std::recursive_mutex>((h)->mu) \
+                                                           : std::unique_lock<std::recursive_mutex>()
 
 #define CKL()                                                                        \
     do {                                                                             \
@@ -770,10 +780,13 @@ struct rl_instance {
     int last_kmax = 4;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timing = false;
+    cudaEvent_t done = nullptr;            // recorded after k_vnd_finalize (rl_vnd_collect waits on it)
+    mutable std::recursive_mutex mu;       // RL_GUARD
     struct GvnsState *gv = nullptr;        // device GVNS state (gvns_impl.cuh)
     double cost_bound = 0.0;               // upper bound of any plan's cost (upload)
     bool cta_long = true;                  // T > 63, few products: CTA per product (k_vnd_cta)
     int skip_mode = 0;                     // slack skip: 0 auto, 1 always, 2 never (A/B)
+    bool force64 = false;                  // variant bit 4: int64 values and costs (A/B)
 };
 
 struct GvnsState;
@@ -819,9 +832,14 @@ static int prepare(rl_instance *h)
                     "instance too large for exact int64 costs (max sum D+R %.3g, cost bound %.3g)",
                     sdr, B);
     h->cost_bound = B;
+    // new instance data: the device GVNS state (F, Fcost, the captured batch
+    // graph and shake scratch sized for the old widths) is stale
+    gvns_free(h->gv);
+    h->gv = nullptr;
     // int32 values only with int32 coefficients (seg_cost<int32, int64>
     // multiplies 32 x 32 -> 64); int32 costs when every plan's cost fits
-    const int vbytes = sdr < std::ldexp(1.0, 28) && Q < std::ldexp(1.0, 30) ? 4 : 8;
+    const int vbytes =
+        !h->force64 && sdr < std::ldexp(1.0, 28) && Q < std::ldexp(1.0, 30) ? 4 : 8;
     const int cbytes = (vbytes == 4 && B < std::ldexp(1.0, 30)) ? 4 : 8;
     if (h->dem && h->vbytes == 4 && vbytes != 4) {
         CK(cudaFree(h->dem));
@@ -892,6 +910,7 @@ static int alloc_instance(rl_instance *h)
     if (e == cudaSuccess) e = cudaMalloc(&h->scan_u8, K * 4);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming);
     if (e != cudaSuccess)
         return fail(RL_ECUDA, "rl_instance_create: %s", cudaGetErrorString(e));
     return ensure_trace(h, 1024, 4);
@@ -936,6 +955,7 @@ extern "C" int rl_instance_update(rl_instance *h, const int64_t *demand, const i
                                   const int64_t *hold_m, const int64_t *hold_r,
                                   const int64_t *unit_m, const int64_t *unit_r)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !demand || !returns || !setup_m || !setup_r || !hold_m || !hold_r || !unit_m ||
         !unit_r)
@@ -961,6 +981,7 @@ extern "C" void rl_instance_destroy(rl_instance *h)
             cudaFree(p);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->done) cudaEventDestroy(h->done);
     if (h->stream)
         cudaStreamDestroy(h->stream);
     if (h->stream2)
@@ -1023,16 +1044,24 @@ static int launch_cfg_cta(rl_instance *h, const void *fn, int64_t nprod, int &gr
 
 extern "C" int rl_instance_set_variant(rl_instance *h, int variant)
 {
+    RL_GUARD(h);
     // bit 0 (two products per warp) was removed: measured slower
-    if (!h || variant < 0 || variant > 11 || (variant & 12) == 12 || (variant & 1))
+    if (!h || variant < 0 || variant > 31 || (variant & 12) == 12 || (variant & 1))
         return fail(RL_EINVAL, "rl_instance_set_variant: bad arguments");
     h->cta_long = (variant & 2) == 0;
     h->skip_mode = (variant & 4) ? 1 : (variant & 8) ? 2 : 0;
+    const bool f64 = (variant & 16) != 0;
+    if (f64 != h->force64) {   // re-pick the widths from the resident int64 rows
+        CK(cudaSetDevice(h->device));
+        h->force64 = f64;
+        return prepare(h);
+    }
     return 0;
 }
 
 extern "C" int rl_instance_info(const rl_instance *h, int64_t *info)
 {
+    RL_GUARD(h);
     if (!h || !info)
         return fail(RL_EINVAL, "rl_instance_info: bad arguments");
     info[0] = h->K;
@@ -1102,6 +1131,7 @@ static int do_costs(rl_instance *h, int64_t lo, int64_t hi, int64_t *d_out)
 extern "C" int rl_product_costs(rl_instance *h, int64_t lo, int64_t hi, const uint8_t *sm,
                                 const uint8_t *sr, int64_t *out)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     int rc = check_range(h, lo, hi);
     if (rc)
@@ -1145,6 +1175,7 @@ extern "C" int rl_scan_products(rl_instance *h, int64_t lo, int64_t hi, const ui
                                 uint8_t *m0, uint8_t *r0, int64_t *p1, uint8_t *m1, uint8_t *r1,
                                 int64_t *evals)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     int rc = check_range(h, lo, hi);
     if (rc)
@@ -1187,6 +1218,7 @@ extern "C" int rl_apply_scan(rl_instance *h, int64_t lo, int64_t hi, const int64
                              const int64_t *p1, const uint8_t *m1, const uint8_t *r1, uint8_t *sm,
                              uint8_t *sr, int64_t *diff)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     int rc = check_range(h, lo, hi);
     if (rc)
@@ -1300,6 +1332,7 @@ static int do_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uint8_t
     CK(cudaEventRecord(h->ev1, st));
     k_vnd_finalize<<<1, 1024, 0, st>>>(h->K, vnd_out(h, 0, h->K, h->ints), h->summary);
     CKL();
+    CK(cudaEventRecord(h->done, st));
     return 0;
 }
 
@@ -1307,6 +1340,7 @@ extern "C" int rl_vnd_device(rl_instance *h, int k_max, const uint8_t *d_sm_in,
                              const uint8_t *d_sr_in, uint8_t *d_sm_out, uint8_t *d_sr_out,
                              void *stream)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h)
         return fail(RL_EINVAL, "null handle");
@@ -1323,13 +1357,17 @@ extern "C" int rl_vnd_device(rl_instance *h, int k_max, const uint8_t *d_sm_in,
 extern "C" int rl_vnd_collect(rl_instance *h, int64_t *trace, int64_t trace_cap, int64_t *n_trace,
                               int64_t *stats)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !stats)
         return fail(RL_EINVAL, "rl_vnd_collect: bad arguments");
     CK(cudaSetDevice(h->device));
-    CK(cudaDeviceSynchronize());
+    // the descent may have been enqueued on a caller's stream: wait for its
+    // finalize only (no device-wide sync: other handles keep running)
+    CK(cudaEventSynchronize(h->done));
     int64_t sum[16];
-    CK(cudaMemcpy(sum, h->summary, sizeof sum, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(sum, h->summary, sizeof sum, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     const int64_t S = sum[2];
@@ -1342,8 +1380,15 @@ extern "C" int rl_vnd_collect(rl_instance *h, int64_t *trace, int64_t trace_cap,
     if (trace && trace_cap > 0) {
         const int64_t m = (n - 1 < trace_cap - 1 ? n - 1 : trace_cap - 1);
         int64_t *dec = new int64_t[m > 0 ? m : 1];
-        if (m > 0)
-            CK(cudaMemcpy(dec, h->trace_dec, m * 8, cudaMemcpyDeviceToHost));
+        if (m > 0) {
+            const cudaError_t e = cudaMemcpyAsync(dec, h->trace_dec, m * 8, cudaMemcpyDeviceToHost,
+                                                  h->stream);
+            const cudaError_t e2 = e == cudaSuccess ? cudaStreamSynchronize(h->stream) : e;
+            if (e2 != cudaSuccess) {
+                delete[] dec;
+                return fail(RL_ECUDA, "rl_vnd_collect: %s", cudaGetErrorString(e2));
+            }
+        }
         trace[0] = sum[1];
         for (int64_t i = 0; i < m; ++i)
             trace[i + 1] = trace[i] - dec[i];
@@ -1365,6 +1410,7 @@ extern "C" int rl_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uin
                       uint8_t *sm_out, uint8_t *sr_out, int64_t *trace, int64_t trace_cap,
                       int64_t *n_trace, int64_t *stats)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h)
         return fail(RL_EINVAL, "null handle");
@@ -1414,14 +1460,16 @@ extern "C" int rl_walk_stats(int64_t *out, int reset)
 extern "C" int rl_vnd_product_stats(rl_instance *h, int32_t *sweeps, int32_t *moves,
                                     int64_t *evals)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !sweeps || !moves || !evals)
         return fail(RL_EINVAL, "rl_vnd_product_stats: bad arguments");
     CK(cudaSetDevice(h->device));
-    CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(sweeps, h->p32, h->K * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(moves, h->p32 + h->K, h->K * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(evals, h->p64 + 2 * h->K, h->K * 8, cudaMemcpyDeviceToHost));
+    CK(cudaEventSynchronize(h->done));
+    CK(cudaMemcpyAsync(sweeps, h->p32, h->K * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(moves, h->p32 + h->K, h->K * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(evals, h->p64 + 2 * h->K, h->K * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     return 0;
 }
 
@@ -1524,6 +1572,7 @@ extern "C" int rl_vnd_host(rl_instance *h, int k_max, const int64_t *demand,
                            uint8_t *sm_out, uint8_t *sr_out, int64_t *trace, int64_t trace_cap,
                            int64_t *n_trace, int64_t *stats)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !demand || !returns || !setup_m || !setup_r || !hold_m || !hold_r || !unit_m ||
         !unit_r || !sm_in || !sr_in || !sm_out || !sr_out || !stats)
@@ -1572,6 +1621,10 @@ extern "C" int rl_vnd_host(rl_instance *h, int k_max, const int64_t *demand,
     CK(cudaEventRecord(h->ev1, s0));
     k_vnd_finalize<<<1, 1024, 0, s0>>>(K, vnd_out(h, 0, K, h->ints), h->summary);
     CKL();
+    CK(cudaEventRecord(h->done, s0));
+    // the instance data changed: the device GVNS state is stale
+    gvns_free(h->gv);
+    h->gv = nullptr;
     int bad = 0;
     unsigned long long hb[2];
     CK(cudaMemcpyAsync(&bad, h->ints + 3, sizeof bad, cudaMemcpyDeviceToHost, s0));
@@ -1602,6 +1655,7 @@ static int do_initial(rl_instance *h, uint8_t *d_sm, uint8_t *d_sr, cudaStream_t
 extern "C" int rl_initial_solution_device(rl_instance *h, uint8_t *d_sm, uint8_t *d_sr,
                                           void *stream)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !d_sm || !d_sr)
         return fail(RL_EINVAL, "rl_initial_solution_device: bad arguments");
@@ -1612,6 +1666,7 @@ extern "C" int rl_initial_solution_device(rl_instance *h, uint8_t *d_sm, uint8_t
 
 extern "C" int rl_initial_solution(rl_instance *h, uint8_t *sm, uint8_t *sr)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !sm || !sr)
         return fail(RL_EINVAL, "rl_initial_solution: bad arguments");
@@ -1639,13 +1694,14 @@ static int do_decode(rl_instance *h, int64_t *d_out, cudaStream_t st)
 extern "C" int rl_decode(rl_instance *h, const uint8_t *sm, const uint8_t *sr, int64_t *x_m,
                          int64_t *x_r, int64_t *y_m, int64_t *y_r, int64_t *cost)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !sm || !sr || !x_m || !x_r || !y_m || !y_r || !cost)
         return fail(RL_EINVAL, "rl_decode: bad arguments");
     CK(cudaSetDevice(h->device));
     const size_t kt = (size_t)h->K * h->T;
     int64_t *d = nullptr;
-    CK(cudaMalloc(&d, (4 * kt + h->K) * 8));
+    CK(cudaMallocAsync((void **)&d, (4 * kt + h->K) * 8, h->stream));
     int rc = 0;
     do {
         cudaError_t e = cudaMemcpyAsync(h->plan, sm, kt, cudaMemcpyHostToDevice, h->stream);
@@ -1666,7 +1722,7 @@ extern "C" int rl_decode(rl_instance *h, const uint8_t *sm, const uint8_t *sr, i
         if (e != cudaSuccess)
             rc = fail(RL_ECUDA, "rl_decode: %s", cudaGetErrorString(e));
     } while (0);
-    cudaFree(d);
+    cudaFreeAsync(d, h->stream);
     return rc;
 }
 
@@ -1735,6 +1791,7 @@ __global__ void k_oracle(int64_t K, int T, const int64_t *dem, const int64_t *re
 
 extern "C" int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uint8_t *sr)
 {
+    RL_GUARD(h);
     (void)cudaGetLastError();
     if (!h || !cost || !sm || !sr)
         return fail(RL_EINVAL, "rl_oracle_optimal: bad arguments");
@@ -1749,7 +1806,7 @@ extern "C" int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uin
     const int64_t K = h->K;
     const int T = h->T;
     unsigned long long *d = nullptr;
-    CK(cudaMalloc(&d, K * 8));
+    CK(cudaMallocAsync((void **)&d, K * 8, h->stream));
     int rc = 0;
     std::vector<unsigned long long> hk((size_t)K);
     do {
@@ -1783,7 +1840,7 @@ extern "C" int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uin
             }
         }
     } while (0);
-    cudaFree(d);
+    cudaFreeAsync(d, h->stream);
     return rc;
 }
 
@@ -1802,31 +1859,36 @@ extern "C" int rl_list_moves(int nbh, int64_t T, const uint8_t *sm_row, const ui
     const size_t words = 2 * cap + 1;
     const size_t bytes = words * 8 + 2 * (size_t)T + 4 * cap;
     uint8_t *d = nullptr;
-    CK(cudaMalloc(&d, bytes));
+    const cudaStream_t st = cudaStreamPerThread;
+    CK(cudaMallocAsync((void **)&d, bytes, st));
     int64_t *dmp0 = (int64_t *)d, *dmp1 = dmp0 + cap, *dn = dmp1 + cap;
     uint8_t *dsm = d + words * 8, *dsr = dsm + T, *db = dsr + T;
     int rc = 0;
-    cudaError_t e = cudaMemcpy(dsm, sm_row, T, cudaMemcpyHostToDevice);
+    cudaError_t e = cudaMemcpyAsync(dsm, sm_row, T, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
-        e = cudaMemcpy(dsr, sr_row, T, cudaMemcpyHostToDevice);
+        e = cudaMemcpyAsync(dsr, sr_row, T, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
-        k_list_moves<<<1, 32, slot_bytes<int32_t, int32_t>((int)T)>>>(
+        k_list_moves<<<1, 32, slot_bytes<int32_t, int32_t>((int)T), st>>>(
             nbh, (int)T, dsm, dsr, dmp0, db, db + cap, dmp1, db + 2 * cap, db + 3 * cap, dn);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess)
-        e = cudaMemcpy(n, dn, 8, cudaMemcpyDeviceToHost);
+        e = cudaMemcpyAsync(n, dn, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+        e = cudaStreamSynchronize(st);
     if (e == cudaSuccess && *n > 0) {
-        e = cudaMemcpy(mp0, dmp0, *n * 8, cudaMemcpyDeviceToHost);
+        e = cudaMemcpyAsync(mp0, dmp0, *n * 8, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess)
-            e = cudaMemcpy(mp1, dmp1, *n * 8, cudaMemcpyDeviceToHost);
+            e = cudaMemcpyAsync(mp1, dmp1, *n * 8, cudaMemcpyDeviceToHost, st);
         uint8_t *outs[4] = {mm0, mr0, mm1, mr1};
         for (int i = 0; i < 4 && e == cudaSuccess; ++i)
-            e = cudaMemcpy(outs[i], db + i * cap, *n, cudaMemcpyDeviceToHost);
+            e = cudaMemcpyAsync(outs[i], db + i * cap, *n, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess)
+            e = cudaStreamSynchronize(st);
     }
     if (e != cudaSuccess)
         rc = fail(RL_ECUDA, "rl_list_moves: %s", cudaGetErrorString(e));
-    cudaFree(d);
+    cudaFreeAsync(d, cudaStreamPerThread);
     return rc;
 }
 

@@ -69,6 +69,32 @@ def combine(trace, stats, group=None, device="cpu"):
     return g_trace, totals
 
 
+def merge_shards(parts, k_max=4):
+    """The job's (trace, totals) from every shard's (trace, stats) in one
+    process -- what ``combine`` computes with collectives (used to pin the
+    multi-rank result on one device and in tests)."""
+    starts = [int(t[0]) for t, _ in parts]
+    decs = [[int(t[i]) - int(t[i + 1]) for i in range(len(t) - 1)] for t, _ in parts]
+    n_pass = max(len(d) for d in decs)
+    vec = [0] * n_pass
+    for d in decs:
+        for i, x in enumerate(d):
+            vec[i] += x
+    start_total = INFEASIBLE if INFEASIBLE in starts else sum(starts)
+    g_trace = [start_total]
+    for d in vec:
+        g_trace.append(g_trace[-1] - d)
+    sweeps = n_pass // k_max
+    ref = sum(int(st.get("evals_reference", 0)) - (len(d) // k_max) * int(st.get("ntot_sum", 0))
+              for d, (_, st) in zip(decs, parts))
+    ntot = sum(int(st.get("ntot_sum", 0)) for _, st in parts)
+    totals = dict(start_cost=start_total, cost=g_trace[-1], sweeps=sweeps,
+                  evals=sum(int(st.get("evals", 0)) for _, st in parts),
+                  moves=sum(int(st.get("moves", 0)) for _, st in parts),
+                  evals_reference=ref + sweeps * ntot)
+    return g_trace, totals
+
+
 def sharded_vnd(inst, plan, k_max=4, group=None, local_vnd=None, device="cpu",
                 gather_plan=True):
     """VND of ``inst`` from ``plan`` with products sharded over the ranks of

@@ -145,3 +145,29 @@ def test_sharded_replicas_equal_reference_gvns(world):
             assert cost == int(data[key + "_cost"]), key
             assert rounds == 6 and shakes == 18
             assert pm == data[key + "_sm"].tobytes() and pr == data[key + "_sr"].tobytes(), key
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_merge_shards_equals_unsharded_reference(world):
+    """sharded.merge_shards (the combine of all shards in one process, used
+    to pin multi-rank results on one device) == one unsharded descent."""
+    from paper_1704_05132_b200.sharded import merge_shards
+    for K, T, seed, kind in CASES:
+        inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=seed,
+                                                 demand_max=30 if T < 20 else 100))
+        if kind == "init":
+            sm, sr = oracle.initial_solution(inst)
+        else:
+            rng = np.random.default_rng(seed)
+            sm, sr = rng.random((K, T)) < 0.5, rng.random((K, T)) < 0.5
+        parts = []
+        for r in range(world):
+            lo, hi = shard_bounds(K, r, world)
+            if hi > lo:
+                _, _, trace, st = _oracle_local_vnd(inst.slice(lo, hi), sm[lo:hi], sr[lo:hi], 4)
+                parts.append((trace, st))
+        g_trace, tot = merge_shards(parts, 4)
+        m, r_, cost, trace, st = oracle.vnd(inst, sm, sr)
+        assert g_trace == trace.tolist() and tot["cost"] == cost
+        assert tot["evals_reference"] == st["evals"] and tot["sweeps"] == st["sweeps"]
+        assert tot["moves"] == st["moves"]

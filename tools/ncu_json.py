@@ -18,7 +18,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr, units, vals = rows[0], rows[1], rows[2]
+hdr, units = rows[0], rows[1]
+kcol = hdr.index("Kernel Name")
+# the VND kernel's row (a capture may hold other launches too)
+vals = next((r for r in rows[2:] if r[kcol].startswith("void k_vnd<")), rows[2])
 get = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
 
 
@@ -42,6 +45,11 @@ summary = {
     "alu_pipe_pct": round(num("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"), 1),
     "fma_pipe_pct": round(num("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"), 1),
     "threads_per_inst": round(num("smsp__thread_inst_executed_per_inst_executed.ratio"), 2),
+    "threads_pred_on_per_inst": round(
+        num("smsp__thread_inst_executed_pred_on_per_inst_executed.ratio"), 2),
+    "sm_clock_mhz": round(float(get["sm__cycles_elapsed.avg.per_second"][0].replace(",", "")) * {
+        "Ghz": 1e3, "GHz": 1e3, "Mhz": 1.0, "MHz": 1.0, "hz": 1e-6, "Hz": 1e-6}.get(
+        get["sm__cycles_elapsed.avg.per_second"][1], 1.0), 1),
     "warps_active_pct": round(num("sm__warps_active.avg.pct_of_peak_sustained_active"), 1),
     "warp_inst": int(num("smsp__inst_executed.sum")),
     "registers": int(num("launch__registers_per_thread")),
