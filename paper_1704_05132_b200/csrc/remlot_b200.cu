@@ -554,6 +554,7 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
     }
 }
 
+#include "lane_vnd.cuh"
 
 // Totals (one block).  summary: 0 final, 1 start, 2 sweeps, 3 evals done,
 // 4 reference-equivalent evals, 5 moves, 6 K, 8 overflow, 9 sum of decreases.
@@ -787,6 +788,9 @@ struct rl_instance {
     bool cta_long = true;                  // T > 63, few products: CTA per product (k_vnd_cta)
     int skip_mode = 0;                     // slack skip: 0 auto, 1 always, 2 never (A/B)
     bool force64 = false;                  // variant bit 4: int64 values and costs (A/B)
+    int lane_mode = 0;                     // lane-per-product kernel: 2 = use it (variant bit 6)
+    int lane_refill = RL_LANE_REFILL_MIN;  // idle lanes that trigger its control step
+    double sdr_max = 0.0;                  // max over products of sum D + sum R
 };
 
 struct GvnsState;
@@ -832,6 +836,7 @@ static int prepare(rl_instance *h)
                     "instance too large for exact int64 costs (max sum D+R %.3g, cost bound %.3g)",
                     sdr, B);
     h->cost_bound = B;
+    h->sdr_max = sdr;
     // new instance data: the device GVNS state (F, Fcost, the captured batch
     // graph and shake scratch sized for the old widths) is stale
     gvns_free(h->gv);
@@ -942,6 +947,8 @@ extern "C" int rl_instance_create(int64_t K, int64_t T, const int64_t *demand,
     rl_instance *h = new rl_instance();
     h->K = K;
     h->T = (int)T;
+    if (const char *e = getenv("RL_LANE_REFILL"))   // A/B of the lane kernel's refill batch
+        h->lane_refill = atoi(e) > 0 ? atoi(e) : h->lane_refill;
     int rc = alloc_instance(h);
     if (!rc) {
         const int64_t *cost[6] = {setup_m, setup_r, hold_m, hold_r, unit_m, unit_r};
@@ -1046,8 +1053,10 @@ extern "C" int rl_instance_set_variant(rl_instance *h, int variant)
 {
     RL_GUARD(h);
     // bit 0 (two products per warp) was removed: measured slower
-    if (!h || variant < 0 || variant > 31 || (variant & 12) == 12 || (variant & 1))
+    if (!h || variant < 0 || variant > 127 || (variant & 12) == 12 || (variant & 1) ||
+        (variant & 96) == 96)
         return fail(RL_EINVAL, "rl_instance_set_variant: bad arguments");
+    h->lane_mode = (variant & 32) ? 1 : (variant & 64) ? 2 : 0;
     h->cta_long = (variant & 2) == 0;
     h->skip_mode = (variant & 4) ? 1 : (variant & 8) ? 2 : 0;
     const bool f64 = (variant & 16) != 0;
@@ -1305,6 +1314,37 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
     if (rc)
         return rc;
     const VndOut o = vnd_out(h, lo, hi, queue);
+    // lane per product (T <= 63, variant bit 6 only): exact, but measured
+    // slower than a warp per product at C3 (29 vs 18.8 ms: latency-bound at
+    // the 13 warps/SM its shared memory allows, plus the tail of ~1.6
+    // products per lane)
+    if (std::is_same<Mask, MaskReg>::value && h->lane_mode == 2) {
+        // 16-bit packed rows when every product's sum D + sum R < 2^15
+        const bool packed = sizeof(V) == 4 && h->sdr_max < 32768.0;
+        const void *fl = packed ? (const void *)k_vnd_lane<V, C, true>
+                                : (const void *)k_vnd_lane<V, C, false>;
+        const size_t lsm = packed ? lane_slot_bytes<V, C, true>(h->T)
+                                  : lane_slot_bytes<V, C, false>(h->T);
+        if (lsm > 48 * 1024)
+            CK(cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fl, 32, lsm));
+        if (occ > 0) {
+            const int64_t want = (nprod + 31) / 32;
+            int64_t cap = h->sms * (int64_t)occ;
+            if (const char *e = getenv("RL_LANE_WARPS_PER_SM"))   // A/B: fewer lanes
+                cap = atoi(e) > 0 && atoi(e) < occ ? (int64_t)h->sms * atoi(e) : cap;
+            const int g = (int)(want < cap ? want : cap);
+            if (packed)
+                k_vnd_lane<V, C, true><<<g, 32, lsm, st>>>(view<V>(h), sm_in, sr_in, sm_out,
+                                                          sr_out, k_max, o, h->lane_refill);
+            else
+                k_vnd_lane<V, C, false><<<g, 32, lsm, st>>>(view<V>(h), sm_in, sr_in, sm_out,
+                                                           sr_out, k_max, o, h->lane_refill);
+            CKL();
+            return 0;
+        }
+    }
     if (cta)
         k_vnd_cta<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
                                                                 sr_out, k_max, o);
@@ -1443,6 +1483,17 @@ extern "C" int rl_vnd(rl_instance *h, int k_max, const uint8_t *sm_in, const uin
 }
 
 #ifdef RL_WALK_STATS
+extern "C" int rl_lane_stats(int64_t *out, int reset)
+{
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpyFromSymbol(out, g_lane_stats, sizeof(g_lane_stats)));
+    if (reset) {
+        static const unsigned long long z[16] = {};
+        CK(cudaMemcpyToSymbol(g_lane_stats, z, sizeof z));
+    }
+    return 0;
+}
+
 extern "C" int rl_walk_stats(int64_t *out, int reset)
 {
     CK(cudaDeviceSynchronize());
@@ -1478,7 +1529,7 @@ extern "C" int rl_vnd_product_stats(rl_instance *h, int32_t *sweeps, int32_t *mo
 // and narrow demand/returns to int32 when that is the stored width.
 __global__ void k_check_narrow(int64_t lo, int64_t hi, int T, int64_t K, const int64_t *dem,
                                const int64_t *ret, const int64_t *c6, int vbytes, int cbytes,
-                               int32_t *dem32, int32_t *ret32, int *bad,
+                               double sdr_lim, int32_t *dem32, int32_t *ret32, int *bad,
                                unsigned long long *bounds)
 {
     const int lane = threadIdx.x & 31;
@@ -1513,7 +1564,7 @@ __global__ void k_check_narrow(int64_t lo, int64_t hi, int T, int64_t K, const i
             const double vlim = std::ldexp(1.0, vbytes == 4 ? 28 : 60);
             const double clim = std::ldexp(1.0, cbytes == 4 ? 30 : 61);
             const bool qok = vbytes == 8 || coef_bound(c, T) < std::ldexp(1.0, 30);
-            if (neg || !(sd + sr < vlim) || !(B < clim) || !qok)
+            if (neg || !(sd + sr < vlim) || !(sd + sr < sdr_lim) || !(B < clim) || !qok)
                 atomicExch(bad, 1);
             atomicMax(&bounds[0], (unsigned long long)__double_as_longlong(sd + sr));
             atomicMax(&bounds[1], (unsigned long long)__double_as_longlong(B));
@@ -1545,8 +1596,11 @@ static int do_vnd_chunks(rl_instance *h, int k_max, int nchunks)
         cudaStream_t st = (c & 1) ? h->stream2 : h->stream;
         const int64_t lo = chunk_lo(K, c, nchunks), hi = chunk_lo(K, c + 1, nchunks);
         CK(cudaStreamWaitEvent(st, h->evc[c], 0));
+        // the decisions taken from the handle's data must hold for the new
+        // rows: exact widths, and 16-bit packed lane rows (launch_vnd_range)
+        const double sdr_lim = h->sdr_max < 32768.0 ? 32768.0 : 1e300;
         k_check_narrow<<<h->sms, 256, 0, st>>>(lo, hi, T, K, h->dem64, h->ret64, h->cost6,
-                                               h->vbytes, h->cbytes, (int32_t *)h->dem,
+                                               h->vbytes, h->cbytes, sdr_lim, (int32_t *)h->dem,
                                                (int32_t *)h->ret, h->ints + 3, h->bounds);
         CKL();
         if (c == 0)

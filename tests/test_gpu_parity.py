@@ -77,7 +77,7 @@ def test_scan_products_golden(small_cases):
             assert ev == oev
 
 
-@pytest.mark.parametrize("variant", [8, 4])
+@pytest.mark.parametrize("variant", [8, 4, 64])
 def test_vnd_golden(small_cases, variant):
     for inst, dev, p in _cases(small_cases):
         dev.set_variant(variant)
@@ -138,7 +138,7 @@ def test_c1_every_lockstep_pass():
     assert st["sweeps"] == int(g["sweeps"]) == 45
 
 
-@pytest.mark.parametrize("variant", [8, 4])
+@pytest.mark.parametrize("variant", [8, 4, 64])
 def test_k1000_vnd_golden(variant):
     g = golden("k1000.npz")
     inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
@@ -160,10 +160,12 @@ def _big():
         return json.load(f)
 
 
-@pytest.mark.parametrize("variant", [8, 4])
+@pytest.mark.parametrize("variant", [8, 4, 64])
 def test_c3_k100000_vnd_golden(variant):
     """BASELINE config 3 at full size: K=100,000, T=52 -- final cost
-    449,100,704,810, full trace and plan hash from the live reference."""
+    449,100,704,810, full trace and plan hash from the live reference
+    (warp-per-product kernel without / with the slack skip, and the
+    lane-per-product kernel)."""
     g = _big()["k100000_t52"]
     inst = generate_instance(GeneratorConfig(products=100000, periods=52, seed=0))
     start = initial_solution(inst)
@@ -213,7 +215,7 @@ def _random_instance(rng, K, T, big=False):
     return Instance(K, T, dem, ret, *c)
 
 
-@pytest.mark.parametrize("variant", [8, 4, 2, 0])
+@pytest.mark.parametrize("variant", [8, 4, 2, 0, 64])
 @pytest.mark.parametrize("seed", range(12))
 def test_fuzz_against_oracle(seed, variant):
     rng = np.random.default_rng(1000 + seed)
