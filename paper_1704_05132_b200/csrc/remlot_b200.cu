@@ -101,8 +101,8 @@ __device__ inline bool tma_ok(const InstView<V> &in, int64_t k)
            !(((uintptr_t)(in.ret + k * in.T)) & 15);
 }
 
-template <typename V, typename C>
-__device__ inline void stage_begin(const Slot<V, C> &s, const InstView<V> &in, int64_t k, int lane)
+template <typename V, typename C, int SB>
+__device__ inline void stage_begin(const Slot<V, C, SB> &s, const InstView<V> &in, int64_t k, int lane)
 {
     if (lane == 0 && tma_ok(in, k)) {
         // order our earlier generic reads of the stage before the async-proxy write
@@ -111,15 +111,15 @@ __device__ inline void stage_begin(const Slot<V, C> &s, const InstView<V> &in, i
     }
 }
 
-template <typename V, typename C>
-__device__ inline void stage_end(const Slot<V, C> &s, const InstView<V> &in, int64_t k, int lane,
+template <typename V, typename C, int SB>
+__device__ inline void stage_end(const Slot<V, C, SB> &s, const InstView<V> &in, int64_t k, int lane,
                                  uint32_t &phase)
 {
     if (tma_ok(in, k)) {
         mbar_wait(s.bar, phase);
         phase ^= 1;
     } else {
-        stage_plain<V, C>(s, in.dem, in.ret, k, in.T, lane);
+        stage_plain(s, in.dem, in.ret, k, in.T, lane);
     }
     __syncwarp();
 }
@@ -136,10 +136,11 @@ __device__ inline double coef_bound(const double *c, int T)
 
 __global__ void k_bounds(int64_t K, int T, const int64_t *dem, const int64_t *ret,
                          const int64_t *c6, unsigned long long *out /* [sumDR, B] as double bits */,
-                         unsigned long long *qmax /* coef_bound, double bits */, int *negative)
+                         unsigned long long *qmax /* coef_bound, double bits */, int *negative,
+                         unsigned long long *sdsr /* max sum D, max sum R, double bits */)
 {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    double sdr = 0.0, B = 0.0, Q = 0.0;
+    double sdr = 0.0, B = 0.0, Q = 0.0, SD = 0.0, SR = 0.0;
     if (k < K) {
         double sd = 0.0, sr = 0.0;
         bool neg = false;
@@ -157,6 +158,8 @@ __global__ void k_bounds(int64_t K, int T, const int64_t *dem, const int64_t *re
         if (neg)
             atomicExch(negative, 1);
         sdr = sd + sr;
+        SD = sd;
+        SR = sr;
         // upper bound of any plan's cost and of every intermediate term
         B = (double)T * (c[0] + c[1]) + (c[4] + c[5]) * sd + (double)T * c[2] * sd +
             (double)T * c[3] * sr;
@@ -165,6 +168,8 @@ __global__ void k_bounds(int64_t K, int T, const int64_t *dem, const int64_t *re
     atomicMax(&out[0], (unsigned long long)__double_as_longlong(sdr));
     atomicMax(&out[1], (unsigned long long)__double_as_longlong(B));
     atomicMax(qmax, (unsigned long long)__double_as_longlong(Q));
+    atomicMax(&sdsr[0], (unsigned long long)__double_as_longlong(SD));
+    atomicMax(&sdsr[1], (unsigned long long)__double_as_longlong(SR));
 }
 
 template <typename V>
@@ -176,8 +181,8 @@ __global__ void k_narrow(int64_t n, const int64_t *src, V *dst)
 }
 
 // Generic "warp per product" prologue: stage rows, costs, prefix, plan.
-template <typename V, typename C, typename Mask>
-__device__ inline C load_product(const Slot<V, C> &s, const InstView<V> &in, const uint8_t *sm,
+template <typename V, typename C, typename Mask, int SB>
+__device__ inline C load_product(const Slot<V, C, SB> &s, const InstView<V> &in, const uint8_t *sm,
                                  const uint8_t *sr, int64_t k, int lane, uint32_t &phase,
                                  ProductCosts<C> &pc, Mask &mk)
 {
@@ -273,8 +278,8 @@ struct VndStats {
 // decreases go to trace_dec[sweep*k_max + nbh-1] when trace_dec != nullptr.
 // Returns the base plan's feasibility (an infeasible product is skipped,
 // _kernels.py:289-290, and counts one sweep).
-template <typename V, typename C, typename Mask, bool Skip>
-__device__ inline bool vnd_product(const Slot<V, C> &s, Mask &mk, int T, const ProductCosts<C> &pc,
+template <typename V, typename C, typename Mask, bool Skip, int SB>
+__device__ inline bool vnd_product(const Slot<V, C, SB> &s, Mask &mk, int T, const ProductCosts<C> &pc,
                                    int k_max, int lane, C &S0, C &S, VndStats &st,
                                    unsigned long long *trace_dec, int64_t cap_sweeps,
                                    int *overflow)
@@ -364,20 +369,24 @@ template <> struct VndMinBlocks<int32_t, int32_t, MaskReg> { static constexpr in
 #endif
 template <> struct VndMinBlocks<int32_t, int64_t, MaskSmem> { static constexpr int value = RL_SMEM_MINB; };
 template <> struct VndMinBlocks<int32_t, int32_t, MaskSmem> { static constexpr int value = RL_SMEM32_MINB; };
-#ifdef RL_VND_MINB
-#define RL_VND_MINB_OF(V, C, M) RL_VND_MINB
-#else
-#define RL_VND_MINB_OF(V, C, M) VndMinBlocks<V, C, M>::value
+#ifndef RL_SMEM16_MINB
+#define RL_SMEM16_MINB 5   // 16-bit rows: 9.8 KB shared per warp at T = 520
 #endif
-template <typename V, typename C, typename Mask, bool Skip>
-__global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask)) k_vnd(InstView<V> in, const uint8_t *sm_in,
+#ifdef RL_VND_MINB
+#define RL_VND_MINB_OF(V, C, M, SB) RL_VND_MINB
+#else
+#define RL_VND_MINB_OF(V, C, M, SB) \
+    (SB == 2 ? RL_SMEM16_MINB : VndMinBlocks<V, C, M>::value)
+#endif
+template <typename V, typename C, typename Mask, bool Skip, int SB = (int)sizeof(V)>
+__global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask, SB)) k_vnd(InstView<V> in, const uint8_t *sm_in,
                                              const uint8_t *sr_in, uint8_t *sm_out,
                                              uint8_t *sr_out, int k_max, VndOut o)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int T = in.T;
-    Slot<V, C> s = carve<V, C>(smem + warp * slot_bytes<V, C>(T), T);
+    Slot<V, C, SB> s = carve<V, C, SB>(smem + warp * slot_bytes<V, C, SB>(T), T);
     if (lane == 0)
         mbar_init(s.bar);
     __syncwarp();
@@ -791,6 +800,8 @@ struct rl_instance {
     int lane_mode = 0;                     // lane-per-product kernel: 2 = use it (variant bit 6)
     int lane_refill = RL_LANE_REFILL_MIN;  // idle lanes that trigger its control step
     double sdr_max = 0.0;                  // max over products of sum D + sum R
+    bool p16 = false;                      // every product's sum D, sum R < 2^16
+    bool no16 = false;                     // variant bit 7: never the 16-bit rows (A/B)
 };
 
 struct GvnsState;
@@ -814,13 +825,14 @@ static int ensure_trace(rl_instance *h, int64_t cap_sweeps, int k_max)
 static int prepare(rl_instance *h)
 {
     const size_t kt = (size_t)h->K * h->T;
-    CK(cudaMemsetAsync(h->bounds, 0, 4 * sizeof(unsigned long long), h->stream));
+    CK(cudaMemsetAsync(h->bounds, 0, 6 * sizeof(unsigned long long), h->stream));
     CK(cudaMemsetAsync(h->ints, 0, 4 * sizeof(int), h->stream));
     const int blk = 256;
     k_bounds<<<(unsigned)((h->K + blk - 1) / blk), blk, 0, h->stream>>>(
-        h->K, h->T, h->dem64, h->ret64, h->cost6, h->bounds, h->bounds + 3, h->ints + 2);
+        h->K, h->T, h->dem64, h->ret64, h->cost6, h->bounds, h->bounds + 3, h->ints + 2,
+        h->bounds + 4);
     CKL();
-    unsigned long long hb[4];
+    unsigned long long hb[6];
     int neg = 0;
     CK(cudaMemcpyAsync(hb, h->bounds, sizeof hb, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(&neg, h->ints + 2, sizeof neg, cudaMemcpyDeviceToHost, h->stream));
@@ -837,6 +849,12 @@ static int prepare(rl_instance *h)
                     sdr, B);
     h->cost_bound = B;
     h->sdr_max = sdr;
+    {
+        double sdm, srm;
+        memcpy(&sdm, &hb[4], 8);
+        memcpy(&srm, &hb[5], 8);
+        h->p16 = sdm < 65536.0 && srm < 65536.0;
+    }
     // new instance data: the device GVNS state (F, Fcost, the captured batch
     // graph and shake scratch sized for the old widths) is stale
     gvns_free(h->gv);
@@ -910,7 +928,7 @@ static int alloc_instance(rl_instance *h)
     if (e == cudaSuccess) e = cudaMalloc(&h->p32, K * 4 * 2);
     if (e == cudaSuccess) e = cudaMalloc(&h->ints, 16 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&h->summary, 16 * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&h->bounds, 4 * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&h->bounds, 8 * 8);
     if (e == cudaSuccess) e = cudaMalloc(&h->scan_i64, K * 8 * 3);
     if (e == cudaSuccess) e = cudaMalloc(&h->scan_u8, K * 4);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
@@ -1006,11 +1024,11 @@ extern "C" void rl_instance_destroy(rl_instance *h)
 // Warp-per-product kernels: kWarpsPerCta warps (one shared-memory slot each)
 // per CTA, fewer when a long horizon's slots do not fit one CTA's opt-in
 // shared memory.  Returns the block size in `block`.
-template <typename V, typename C>
+template <typename V, typename C, int SB = (int)sizeof(V)>
 static int launch_cfg(rl_instance *h, const void *fn, int64_t nprod, int &grid, size_t &smem,
                       int &block)
 {
-    const size_t slot = slot_bytes<V, C>(h->T);
+    const size_t slot = slot_bytes<V, C, SB>(h->T);
     int nw = kWarpsPerCta;
     while (nw > 1 && (size_t)nw * slot > (size_t)h->smem_optin)
         --nw;
@@ -1053,10 +1071,11 @@ extern "C" int rl_instance_set_variant(rl_instance *h, int variant)
 {
     RL_GUARD(h);
     // bit 0 (two products per warp) was removed: measured slower
-    if (!h || variant < 0 || variant > 127 || (variant & 12) == 12 || (variant & 1) ||
+    if (!h || variant < 0 || variant > 255 || (variant & 12) == 12 || (variant & 1) ||
         (variant & 96) == 96)
         return fail(RL_EINVAL, "rl_instance_set_variant: bad arguments");
     h->lane_mode = (variant & 32) ? 1 : (variant & 64) ? 2 : 0;
+    h->no16 = (variant & 128) != 0;
     h->cta_long = (variant & 2) == 0;
     h->skip_mode = (variant & 4) ? 1 : (variant & 8) ? 2 : 0;
     const bool f64 = (variant & 16) != 0;
@@ -1306,11 +1325,19 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
     // the slack skip exists for register rows only: Skip=true is never
     // instantiated for shared-memory rows
     constexpr bool kReg = std::is_same<Mask, MaskReg>::value;
-    const void *fn = cta ? (const void *)k_vnd_cta<V, C>
+    // 16-bit {cd, cr} / xin rows for long horizons when every product's sum D
+    // and sum R < 2^16 (upload proof): 9.8 instead of 12.9 KB per warp at
+    // T = 520, 5 instead of 4 CTAs per SM
+    constexpr bool k16ok = !kReg && std::is_same<V, int32_t>::value &&
+                           std::is_same<C, int64_t>::value;
+    const bool p16 = k16ok && !cta && h->p16 && !h->no16;
+    const void *fn = cta    ? (const void *)k_vnd_cta<V, C>
+                     : p16  ? (const void *)k_vnd<V, C, Mask, false, k16ok ? 2 : (int)sizeof(V)>
                      : skip ? (const void *)k_vnd<V, C, Mask, kReg>
                             : (const void *)k_vnd<V, C, Mask, false>;
     int rc = cta ? launch_cfg_cta<V, C>(h, fn, nprod, grid, smem)
-                 : launch_cfg<V, C>(h, fn, nprod, grid, smem, block);
+             : p16 ? launch_cfg<V, C, k16ok ? 2 : (int)sizeof(V)>(h, fn, nprod, grid, smem, block)
+                   : launch_cfg<V, C>(h, fn, nprod, grid, smem, block);
     if (rc)
         return rc;
     const VndOut o = vnd_out(h, lo, hi, queue);
@@ -1348,6 +1375,9 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
     if (cta)
         k_vnd_cta<V, C><<<grid, kWarpsPerCta * 32, smem, st>>>(view<V>(h), sm_in, sr_in, sm_out,
                                                                 sr_out, k_max, o);
+    else if (p16)
+        k_vnd<V, C, Mask, false, k16ok ? 2 : (int)sizeof(V)><<<grid, block, smem, st>>>(
+            view<V>(h), sm_in, sr_in, sm_out, sr_out, k_max, o);
     else if (skip)
         k_vnd<V, C, Mask, kReg><<<grid, block, smem, st>>>(view<V>(h), sm_in, sr_in,
                                                             sm_out, sr_out, k_max, o);
@@ -1529,7 +1559,8 @@ extern "C" int rl_vnd_product_stats(rl_instance *h, int32_t *sweeps, int32_t *mo
 // and narrow demand/returns to int32 when that is the stored width.
 __global__ void k_check_narrow(int64_t lo, int64_t hi, int T, int64_t K, const int64_t *dem,
                                const int64_t *ret, const int64_t *c6, int vbytes, int cbytes,
-                               double sdr_lim, int32_t *dem32, int32_t *ret32, int *bad,
+                               double sdr_lim, double p16_lim, int32_t *dem32, int32_t *ret32,
+                               int *bad,
                                unsigned long long *bounds)
 {
     const int lane = threadIdx.x & 31;
@@ -1564,7 +1595,8 @@ __global__ void k_check_narrow(int64_t lo, int64_t hi, int T, int64_t K, const i
             const double vlim = std::ldexp(1.0, vbytes == 4 ? 28 : 60);
             const double clim = std::ldexp(1.0, cbytes == 4 ? 30 : 61);
             const bool qok = vbytes == 8 || coef_bound(c, T) < std::ldexp(1.0, 30);
-            if (neg || !(sd + sr < vlim) || !(sd + sr < sdr_lim) || !(B < clim) || !qok)
+            if (neg || !(sd + sr < vlim) || !(sd + sr < sdr_lim) || !(sd < p16_lim) ||
+                !(sr < p16_lim) || !(B < clim) || !qok)
                 atomicExch(bad, 1);
             atomicMax(&bounds[0], (unsigned long long)__double_as_longlong(sd + sr));
             atomicMax(&bounds[1], (unsigned long long)__double_as_longlong(B));
@@ -1599,8 +1631,10 @@ static int do_vnd_chunks(rl_instance *h, int k_max, int nchunks)
         // the decisions taken from the handle's data must hold for the new
         // rows: exact widths, and 16-bit packed lane rows (launch_vnd_range)
         const double sdr_lim = h->sdr_max < 32768.0 ? 32768.0 : 1e300;
+        const double p16_lim = h->p16 ? 65536.0 : 1e300;
         k_check_narrow<<<h->sms, 256, 0, st>>>(lo, hi, T, K, h->dem64, h->ret64, h->cost6,
-                                               h->vbytes, h->cbytes, sdr_lim, (int32_t *)h->dem,
+                                               h->vbytes, h->cbytes, sdr_lim, p16_lim,
+                                               (int32_t *)h->dem,
                                                (int32_t *)h->ret, h->ints + 3, h->bounds);
         CKL();
         if (c == 0)

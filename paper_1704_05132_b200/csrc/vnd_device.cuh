@@ -127,11 +127,70 @@ struct XCStore<V, C, true> {
     __device__ void *base() const { return c; }
 };
 
+// {cd[t], cr[t+1]} per period.  SB = stored bytes per value: sizeof(V)
+// stores DR<V> pairs; SB = 2 (int32 values with every product's sum D and sum
+// R below 2^16, proved at upload) stores the two 16-bit halves of one word
+// (the long-horizon kernel's occupancy is bounded by shared memory).
+template <typename V, int SB>
+struct DRStore {
+    DR<V> *p;
+    __host__ __device__ static size_t bytes(int n) { return (size_t)n * sizeof(DR<V>); }
+    __device__ void carve(unsigned char *b) { p = (DR<V> *)b; }
+    __device__ DR<V> operator[](int i) const { return p[i]; }
+    __device__ void set_d(int i, V v) const { p[i].d = v; }
+    __device__ void set_r(int i, V v) const { p[i].r = v; }
+};
+template <typename V>
+struct DRStore<V, 2> {
+    uint32_t *p;
+    __host__ __device__ static size_t bytes(int n) { return (size_t)n * 4; }
+    __device__ void carve(unsigned char *b) { p = (uint32_t *)b; }
+    __device__ DR<V> operator[](int i) const
+    {
+        const uint32_t w = p[i];
+        return DR<V>{V(w & 0xffffu), V(w >> 16)};
+    }
+    __device__ void set_d(int i, V v) const { ((uint16_t *)p)[2 * i] = (uint16_t)v; }
+    __device__ void set_r(int i, V v) const { ((uint16_t *)p)[2 * i + 1] = (uint16_t)v; }
+};
+
+// {cpre, xin} with a 16-bit xin (SB = 2; xin <= sum R < 2^16)
 template <typename V, typename C>
+struct XCStore16 {
+    C *c;
+    uint16_t *x;
+    __host__ __device__ static size_t bytes(int T)
+    {
+        return ((size_t)T * sizeof(C) + 15) / 16 * 16 + (size_t)T * 2;
+    }
+    __device__ void carve(unsigned char *b, int T)
+    {
+        c = (C *)b;
+        x = (uint16_t *)(b + ((size_t)T * sizeof(C) + 15) / 16 * 16);
+    }
+    __device__ XC<V, C> operator[](int i) const
+    {
+        XC<V, C> e;
+        e.c = c[i];
+        e.x = V(x[i]);
+        return e;
+    }
+    __device__ void set(int i, V xv, C cv) const
+    {
+        x[i] = (uint16_t)xv;
+        c[i] = cv;
+    }
+    __device__ void add_c(int i, C d) const { c[i] += d; }
+    __device__ void *base() const { return c; }
+};
+template <typename V, typename C, int SB> struct XCStoreOf { using type = XCStore<V, C>; };
+template <typename V, typename C> struct XCStoreOf<V, C, 2> { using type = XCStore16<V, C>; };
+
+template <typename V, typename C, int SB = (int)sizeof(V)>
 struct Slot {
     V *stage, *slk;
-    DR<V> *dr;
-    XCStore<V, C> xc;
+    DRStore<V, SB> dr;
+    typename XCStoreOf<V, C, SB>::type xc;
     uint16_t *nx;       // T > 63: next setup >= t of the base plan and its kind
     uint32_t *bm, *br, *bs;
     uint16_t *mv;
@@ -153,41 +212,42 @@ constexpr int kSlackLevels = 16;   // lm[j] = slack < 2^j (j < 16), lm[16] = all
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-template <typename V, typename C>
+template <typename V, typename C, int SB = (int)sizeof(V)>
 __host__ __device__ inline size_t slot_bytes(int T)
 {
     const int NW = (T + 31) >> 5;
     size_t b = 0;
-    b += align16((size_t)(T + 1) * sizeof(DR<V>));      // dr
-    b += align16(XCStore<V, C>::bytes(T + 1));         // xc (+ the end entry xc[T])
+    b += align16(DRStore<V, SB>::bytes(T + 1));                      // dr
+    b += align16(XCStoreOf<V, C, SB>::type::bytes(T + 1));          // xc (+ the end entry xc[T])
     b += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));   // slk (register-mask path only)
     b += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(int16_t));   // nx
     b += align16(3 * (size_t)NW * sizeof(uint32_t));
     b += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
-    b += align16((kSlackLevels + 2) * 8);        // lm
+    b += align16((T <= 63 ? kSlackLevels + 2 : 0) * 8);   // lm (register-mask skip only)
     b += 16;                                     // mbarrier
     return b;
 }
 
-template <typename V, typename C>
-__device__ inline Slot<V, C> carve(unsigned char *base, int T)
+template <typename V, typename C, int SB = (int)sizeof(V)>
+__device__ inline Slot<V, C, SB> carve(unsigned char *base, int T)
 {
     const int NW = (T + 31) >> 5;
-    Slot<V, C> s;
+    Slot<V, C, SB> s;
     unsigned char *p = base;
-    s.dr = (DR<V> *)p; p += align16((size_t)(T + 1) * sizeof(DR<V>));
-    s.xc.carve(p, T + 1); p += align16(XCStore<V, C>::bytes(T + 1));
+    s.dr.carve(p); p += align16(DRStore<V, SB>::bytes(T + 1));
+    s.xc.carve(p, T + 1); p += align16(XCStoreOf<V, C, SB>::type::bytes(T + 1));
     // the staged demand/returns rows (2T x V <= the xc area) are consumed by
     // build_prefix before base_pass first writes xc
     s.stage = (V *)s.xc.base();
-    static_assert(sizeof(C) + sizeof(V) >= 2 * sizeof(V), "stage must fit in xc");
+    static_assert(SB == 2 ? sizeof(C) + 2 >= 2 * sizeof(V) : sizeof(C) + sizeof(V) >= 2 * sizeof(V),
+                  "stage must fit in xc");
     s.slk = (V *)p;   p += align16((size_t)(T <= 63 ? T : 0) * sizeof(V));
     s.nx = (uint16_t *)p; p += align16((size_t)(T > 63 ? T + 1 : 0) * sizeof(uint16_t));
     s.bm = (uint32_t *)p;
     s.br = s.bm + NW;
     s.bs = s.br + NW; p += align16(3 * (size_t)NW * sizeof(uint32_t));
     s.mv = (uint16_t *)p; p += align16((size_t)(2 * T + 2) * sizeof(uint16_t));
-    s.lm = (uint64_t *)p; p += align16((kSlackLevels + 2) * 8);
+    s.lm = (uint64_t *)p; p += align16((T <= 63 ? kSlackLevels + 2 : 0) * 8);
     s.bar = (uint64_t *)p;
     return s;
 }
@@ -465,8 +525,8 @@ template <> struct PatchOf<MaskReg> {
 };
 
 // Plan row bytes (bool K x T, plan.py:22-29) -> bit rows.
-template <typename V, typename C>
-__device__ inline MaskSmem load_rows(const Slot<V, C> &s, MaskSmem, const uint8_t *sm,
+template <typename V, typename C, int SB>
+__device__ inline MaskSmem load_rows(const Slot<V, C, SB> &s, MaskSmem, const uint8_t *sm,
                                      const uint8_t *sr, int64_t k, int T, int lane)
 {
     const uint8_t *a = sm + k * (int64_t)T, *b = sr + k * (int64_t)T;
@@ -484,8 +544,8 @@ __device__ inline MaskSmem load_rows(const Slot<V, C> &s, MaskSmem, const uint8_
     return MaskSmem{s.bm, s.br, s.bs, s.nx, T};
 }
 
-template <typename V, typename C>
-__device__ inline MaskReg load_rows(const Slot<V, C> &, MaskReg, const uint8_t *sm,
+template <typename V, typename C, int SB>
+__device__ inline MaskReg load_rows(const Slot<V, C, SB> &, MaskReg, const uint8_t *sm,
                                     const uint8_t *sr, int64_t k, int T, int lane)
 {
     const uint8_t *a = sm + k * (int64_t)T, *b = sr + k * (int64_t)T;
@@ -552,14 +612,14 @@ __device__ inline bool seg_cost<int32_t, int64_t>(int32_t cdu, int32_t cru, int3
 // ------------------------------------------------------------ staging
 
 // Prefix sums of the staged rows into cd/cr; returns K0 (warp-uniform).
-template <typename V, typename C>
-__device__ inline C build_prefix(const Slot<V, C> &s, int T, const ProductCosts<C> &pc, int lane)
+template <typename V, typename C, int SB>
+__device__ inline C build_prefix(const Slot<V, C, SB> &s, int T, const ProductCosts<C> &pc, int lane)
 {
     V carry_d = 0, carry_r = 0;
     C sum_cd = 0, sum_cr = 0;   // sum_t CD[t], sum_t CR[t] (inclusive prefixes)
     if (lane == 0) {
-        s.dr[0].d = 0;
-        s.dr[T].r = 0;   // cr[T+1]: never used, kept defined
+        s.dr.set_d(0, V(0));
+        s.dr.set_r(T, V(0));   // cr[T+1]: never used, kept defined
     }
     for (int base = 0; base < T; base += 32) {
         const int t = base + lane;
@@ -576,8 +636,8 @@ __device__ inline C build_prefix(const Slot<V, C> &s, int T, const ProductCosts<
         d += carry_d;
         r += carry_r;
         if (t < T) {
-            s.dr[t + 1].d = d;
-            s.dr[t].r = r;
+            s.dr.set_d(t + 1, d);
+            s.dr.set_r(t, r);
             sum_cd += C(d);
             sum_cr += C(r);
         }
@@ -594,8 +654,8 @@ __device__ inline C build_prefix(const Slot<V, C> &s, int T, const ProductCosts<
 }
 
 // Plain coalesced staging (fallback when TMA alignment does not hold).
-template <typename V, typename C>
-__device__ inline void stage_plain(const Slot<V, C> &s, const V *dem, const V *ret, int64_t k,
+template <typename V, typename C, int SB>
+__device__ inline void stage_plain(const Slot<V, C, SB> &s, const V *dem, const V *ret, int64_t k,
                                    int T, int lane)
 {
     const V *d = dem + k * (int64_t)T, *r = ret + k * (int64_t)T;
@@ -612,8 +672,8 @@ __device__ inline void stage_plain(const Slot<V, C> &s, const V *dem, const V *r
 // feasibility and S = sum of segment costs (warp-uniform).  Lane l owns the
 // periods [l*L, l*L+L).  Step 1 composes the (min,+) maps of its setups,
 // a warp scan gives every lane its entering X, step 2 walks the segments.
-template <typename V, typename C, typename Mask, bool Skip = false>
-__device__ inline bool base_pass(const Slot<V, C> &s, const Mask &mk, int T,
+template <typename V, typename C, typename Mask, bool Skip = false, int SB = 4>
+__device__ inline bool base_pass(const Slot<V, C, SB> &s, const Mask &mk, int T,
                                  const ProductCosts<C> &pc, int lane, C &S)
 {
     if constexpr (std::is_same<Mask, MaskSmem>::value)
@@ -861,8 +921,8 @@ __device__ inline RegMoveMasks reg_move_masks(const MaskReg &mk)
     return r;
 }
 
-template <typename V, typename C>
-__device__ inline int enumerate_moves(const Slot<V, C> &s, const MaskReg &mk, int nbh, int T,
+template <typename V, typename C, int SB>
+__device__ inline int enumerate_moves(const Slot<V, C, SB> &s, const MaskReg &mk, int nbh, int T,
                                       int lane)
 {
     if (nbh <= 2)
@@ -945,8 +1005,8 @@ __device__ inline int warp_excl_scan(int x, int lane, int &total)
     return incl - x;
 }
 
-template <typename V, typename C>
-__device__ inline int enumerate_moves(const Slot<V, C> &s, const MaskSmem &mk, int nbh, int T,
+template <typename V, typename C, int SB>
+__device__ inline int enumerate_moves(const Slot<V, C, SB> &s, const MaskSmem &mk, int nbh, int T,
                                       int lane)
 {
     if (nbh <= 2)
@@ -1013,8 +1073,8 @@ __device__ inline int enumerate_moves(const Slot<V, C> &s, const MaskSmem &mk, i
     return orr;
 }
 
-template <typename V, typename C, typename Mask>
-__device__ inline int enumerate_moves_ballot(const Slot<V, C> &s, const Mask &mk, int nbh, int T,
+template <typename V, typename C, typename Mask, int SB>
+__device__ inline int enumerate_moves_ballot(const Slot<V, C, SB> &s, const Mask &mk, int nbh, int T,
                                              int lane)
 {
     if (nbh <= 2)
@@ -1063,8 +1123,8 @@ __device__ inline void warp_argmin(C &best, int &key)
 // setup u of its candidate plan with entering X, the candidate's segment
 // costs so far in acc, and cd[u], cr[u+1] carried from the previous step
 // (each step loads one {cd, cr} pair and one {cpre, xin} pair).
-template <typename V, typename C, typename Mask, bool Skip = false>
-__device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
+template <typename V, typename C, typename Mask, bool Skip = false, int SB = 4>
+__device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T,
                                   const ProductCosts<C> &pc, C S, int nbh, int n, int lane,
                                   int wi, int nw, C &best, int &key)
 {
@@ -1232,8 +1292,8 @@ __device__ inline void walk_moves(const Slot<V, C> &s, const Mask &mk, int T,
 #endif
 }
 
-template <typename V, typename C, typename Mask, bool Skip = false>
-__device__ inline PassResult scan_pass(const Slot<V, C> &s, const Mask &mk, int T,
+template <typename V, typename C, typename Mask, bool Skip = false, int SB = 4>
+__device__ inline PassResult scan_pass(const Slot<V, C, SB> &s, const Mask &mk, int T,
                                        const ProductCosts<C> &pc, C S, int nbh, int lane,
                                        C &best_out)
 {
