@@ -172,6 +172,43 @@ def cpu_gvns_reference(threads, workers=2, budget_s=10.0):
                       "Philox restatement) + C oracle VND, one host thread per worker"}
 
 
+def sharded_c5(torch, dist, coll, rank, rounds=40):
+    """BASELINE config 5 on the job's ranks: sharded_gvns with W=1,024 over
+    K=1000 T=52 (seed 0): bit-exactness against the W1024_R2 golden, then
+    rounds/s of a `rounds`-round run (wall clock around the call, device
+    synchronised, max over ranks)."""
+    from paper_1704_05132_b200 import GeneratorConfig, SolverConfig, generate_instance
+    from paper_1704_05132_b200.sharded import sharded_gvns
+    inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+    out = {"workers": 1024, "products": 1000, "periods": 52}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "gvns_c5.json")) as f:
+            g = json.load(f)["W1024_R2"]
+    except (OSError, KeyError, ValueError):
+        g = None
+    res = sharded_gvns(inst, SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=1024,
+                                          seed=0, max_rounds=2))
+    if g is not None:
+        import hashlib
+        h = hashlib.sha256()
+        h.update(np.packbits(res.plan.setup_m).tobytes())
+        h.update(np.packbits(res.plan.setup_r).tobytes())
+        out["bit_exact_W1024_R2"] = res.cost == g["cost"] and h.hexdigest() == g["plan_sha"]
+    cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=1024, seed=0, max_rounds=rounds)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = sharded_gvns(inst, cfg)
+    torch.cuda.synchronize()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=coll)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    sec = float(dt[0])
+    out.update(rounds=res.rounds, seconds=sec, rounds_per_s=res.rounds / sec,
+               shakes_per_s=res.shake_calls / sec, best_cost=res.cost,
+               timing="wall clock around sharded_gvns, device-synchronised, max over ranks")
+    return out
+
+
 def hbm_bytes(wl):
     """Algorithmic HBM bytes of one VND launch per GPU:
     int32 D, R rows + six int64 cost vectors + plan in/out bytes."""
@@ -430,6 +467,14 @@ def main():
         other = measure(K0 if args.scaling == "weak" else K0 * world, args.steps, args.warmup,
                         False)
 
+    # ---- BASELINE config 5 across the ranks: 1,024 replicas of K=1000 T=52
+    # (sharded.sharded_gvns: worker blocks per rank, speculative batches, one
+    # all-gather per batch), parity against the live reference's round-capped
+    # golden and rounds/s over a longer run
+    c5 = None
+    if world > 1 and not args.no_extra:
+        c5 = sharded_c5(torch, dist, coll, rank)
+
     line = None
     if rank == 0:
         value = m["value"]
@@ -479,6 +524,8 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "roofline": roof,
         }
+        if c5 is not None:
+            line["c5_sharded"] = c5
         if other is not None:
             line["strong" if args.scaling == "weak" else "weak"] = {
                 "products": other["K"], "value": other["value"], "unit": "evals/s",

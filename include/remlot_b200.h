@@ -207,6 +207,18 @@ int rl_gvns_state(rl_instance *h, int which, uint8_t *sm, uint8_t *sr, int64_t *
  * device memory) the incumbent. */
 int rl_gvns_candidate(rl_instance *h, uint8_t *d_plan, int64_t *best);
 int rl_gvns_import(rl_instance *h, const uint8_t *d_plan, int64_t cost);
+/* Sharded rounds in speculative batches (one collective per batch): after
+ * rl_gvns_begin_batch(h, W_local, B, ...) and rl_gvns_set_strength(h, k),
+ * rl_gvns_run_local runs rounds round0 .. round0+nb-1 (nb <= B) of this
+ * rank's worker block, each shaking the incumbent with the strength it has
+ * if the rounds before it do not improve, without acceptance; out[3j..3j+2]
+ * = round j's best (cost, global worker, local slot) for j < *n_out (fewer
+ * than nb when the fallback slots ran out; the caller re-runs the rest).
+ * rl_gvns_export copies round jr's best candidate (2KT bytes, device memory)
+ * for the winner's broadcast; the job's winner is adopted with
+ * rl_gvns_import.  Both synchronous. */
+int rl_gvns_run_local(rl_instance *h, int64_t round0, int nb, int64_t *out, int64_t *n_out);
+int rl_gvns_export(rl_instance *h, int jr, uint8_t *d_plan);
 /* Test hook: numpy-exact Philox stream of SeedSequence((seed, round,
  * worker)) on the device: out = 4 raw next64, choice(pop, size,
  * replace=False), shuffle of [1, 4, 7, ...] (shuffle_n), one more next64. */

@@ -57,10 +57,27 @@ class OracleRounds:
     def initial_solution(self):
         return self.init[0].copy(), self.init[1].copy()
 
-    def begin(self, workers, worker_offset, config, sm, sr):
+    def begin(self, workers, worker_offset, config, sm, sr, batch=1):
         self.W, self.w0, self.cfg = workers, worker_offset, config
         self.sm, self.sr = np.asarray(sm, bool).copy(), np.asarray(sr, bool).copy()
+        self.last = []
         return oracle.evaluate(self.oi, self.sm, self.sr)
+
+    def run_local(self, round0, strength, nb):
+        """Rounds round0 .. round0+nb-1 from the current incumbent with the
+        strengths of a non-improving run (sharded_gvns batches)."""
+        self.last = []
+        k = strength
+        for j in range(nb):
+            self.last.append(self.round(round0 + j, k))
+            k = 1 if k >= self.cfg.k_max else k + 1
+        return [(c, w) for c, w, _ in self.last]
+
+    def export(self, jr):
+        return self.last[jr][2]
+
+    def plan_buffer(self):
+        return self.torch.zeros(2 * self.K * self.T, dtype=self.torch.uint8)
 
     def round(self, round_index, strength):
         best = None

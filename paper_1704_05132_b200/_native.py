@@ -28,6 +28,7 @@ EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_vnd_product_stats",
            "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_oracle_optimal", "rl_int_peak", "rl_gvns_begin", "rl_gvns_begin_batch", "rl_gvns_set_strength",
            "rl_gvns_round", "rl_gvns_run", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
+           "rl_gvns_run_local", "rl_gvns_export",
            "rl_rng_probe", "rl_launch_count", "rl_generate_instance", "rl_instance_download",
            "rl_last_error")
 
@@ -76,6 +77,8 @@ def load():
         "rl_gvns_run": (I, [P, I64]),
         "rl_gvns_candidate": (I, [P, P, P]),
         "rl_gvns_import": (I, [P, P, I64]),
+        "rl_gvns_run_local": (I, [P, I64, I, P, P]),
+        "rl_gvns_export": (I, [P, I, P]),
         "rl_gvns_set_strength": (I, [P, I64]),
         "rl_gvns_round": (I, [P, I64, I]),
         "rl_gvns_state": (I, [P, I, P, P, P]),
@@ -308,6 +311,17 @@ class DeviceInstance:
         check(load().rl_gvns_candidate(self.h, ctypes.c_void_p(d_plan_ptr) if d_plan_ptr else None,
                                        ptr(best)), "rl_gvns_candidate")
         return int(best[0]), int(best[1])
+
+    def gvns_run_local(self, round0, nb):
+        """Local speculative batch of rounds round0.. (no acceptance): the
+        per-round bests [(cost, global worker)] with valid results."""
+        out = np.zeros(3 * nb, np.int64)
+        n = np.zeros(1, np.int64)
+        check(load().rl_gvns_run_local(self.h, round0, nb, ptr(out), ptr(n)), "rl_gvns_run_local")
+        return [(int(out[3 * j]), int(out[3 * j + 1])) for j in range(int(n[0]))]
+
+    def gvns_export(self, jr, d_plan_ptr):
+        check(load().rl_gvns_export(self.h, jr, ctypes.c_void_p(d_plan_ptr)), "rl_gvns_export")
 
     def gvns_import(self, d_plan_ptr, cost):
         check(load().rl_gvns_import(self.h, ctypes.c_void_p(d_plan_ptr), cost), "rl_gvns_import")

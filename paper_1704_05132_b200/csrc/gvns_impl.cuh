@@ -46,6 +46,7 @@ struct GvnsArgs {
     int64_t *fbdiff;                  // fb_slots x pop
     int64_t *fbpcost;                 // fb_slots x K
     int *queue;
+    int64_t *rbest;                   // B x 3: per batch round best (cost, global worker, slot)
 };
 
 enum {
@@ -62,6 +63,7 @@ enum {
     GV_NB,        // rounds of the next batch (adaptive, <= B)
     GV_NTASK,     // compact VND tasks appended by k_shake (reset by the join)
     GV_FB_TRUNC,  // B - (first batch round whose fallback found no slot), 0 = none
+    GV_LOCAL_NB,  // rounds of the last local batch (mode 2) with valid bests
     GV_FBCOST0,   // fb_slots entries follow
 };
 
@@ -565,6 +567,8 @@ __global__ void k_gvns_join(GvnsArgs g, int mode, int64_t round_arg, int64_t max
     if (nb == 0) {
         for (int i = threadIdx.x; i < g.fb_slots; i += blockDim.x)
             g.scal[GV_FBCOST0 + i] = 0;
+        if (mode == 2 && threadIdx.x == 0)
+            g.scal[GV_LOCAL_NB] = 0;
         return;
     }
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -626,6 +630,20 @@ __global__ void k_gvns_join(GvnsArgs g, int mode, int64_t round_arg, int64_t max
         }
     }
     __syncthreads();
+    if (mode == 2) {   // local batch of a sharded run: report, do not accept
+        if (tid < nb) {
+            g.rbest[3 * tid] = s_cost[tid];
+            g.rbest[3 * tid + 1] = g.w0 + s_w[tid] % g.Wr;
+            g.rbest[3 * tid + 2] = s_w[tid];
+        }
+        if (tid == 0)
+            g.scal[GV_LOCAL_NB] = nb;
+        // the fallback plan costs were read above; the plans stay for export
+        __syncthreads();
+        for (int i = tid; i < g.fb_slots; i += blockDim.x)
+            g.scal[GV_FBCOST0 + i] = 0;
+        return;
+    }
     if (tid == 0) {
         int acc = 0, win = 0, used = nb;
         if (mode == 1) {
@@ -851,6 +869,7 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
         if (e == cudaSuccess) e = gv_alloc(gs, &a.fbdiff, (size_t)a.fb_slots * pop * 8);
         if (e == cudaSuccess) e = gv_alloc(gs, &a.fbpcost, (size_t)a.fb_slots * K * 8);
         if (e == cudaSuccess) e = gv_alloc(gs, &a.queue, 16);
+        if (e == cudaSuccess) e = gv_alloc(gs, &a.rbest, (size_t)batch * 3 * 8);
         if (e != cudaSuccess) {
             gvns_free(gs);
             h->gv = nullptr;
@@ -1063,6 +1082,77 @@ extern "C" int rl_gvns_import(rl_instance *h, const uint8_t *d_plan, int64_t cos
     int64_t scal[4] = {cost, cost, 0, 1};   // inc cost, Ftot, (strength kept), inc_is_F
     CK(cudaMemcpyAsync(&a.scal[GV_INC_COST], &scal[0], 16, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(&a.scal[GV_INC_IS_F], &scal[3], 8, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return 0;
+}
+
+// Candidate of batch round jr of the last local batch (mode 2): F with the
+// round's best worker's touched rows, or its fallback plan (one block).
+__global__ void k_gvns_export(GvnsArgs g, int jr, uint8_t *dst)
+{
+    const int w = (int)g.rbest[3 * jr + 2];
+    const int tid = threadIdx.x;
+    const int64_t KT2 = 2 * g.KT;
+    if (g.fb[w]) {
+        const uint8_t *src = g.fbplan + (int64_t)g.fbslot[w] * KT2;
+        for (int64_t i = tid; i < KT2; i += blockDim.x)
+            dst[i] = src[i];
+        return;
+    }
+    for (int64_t i = tid; i < KT2; i += blockDim.x)
+        dst[i] = g.F[i];
+    __syncthreads();
+    const int NW = g.NW, T = g.T, n = g.tn[w];
+    for (int64_t q = tid; q < (int64_t)n * T; q += blockDim.x) {
+        const int j = (int)(q / T), t = (int)(q % T);
+        const int64_t k = g.tp[(int64_t)w * g.tcap + j];
+        const uint32_t *row = g.tw + ((int64_t)w * g.tcap + j) * 2 * NW;
+        dst[k * T + t] = (row[t >> 5] >> (t & 31)) & 1u;
+        dst[g.KT + k * T + t] = (row[NW + (t >> 5)] >> (t & 31)) & 1u;
+    }
+}
+
+// Sharded replicas in speculative batches (sharded.sharded_gvns): rounds
+// round0 .. round0 + nb - 1 (nb <= the begin's batch) with this rank's
+// worker block, each shaking the incumbent with the strength it has if the
+// rounds before it do not improve (strength set by rl_gvns_set_strength);
+// no acceptance.  out[3j .. 3j+2] = round j's best (cost, global worker,
+// local slot); *n_out = rounds with valid bests (fewer when fallback slots
+// ran out: the rest are re-run by the caller).  Synchronous.
+extern "C" int rl_gvns_run_local(rl_instance *h, int64_t round0, int nb, int64_t *out,
+                                 int64_t *n_out)
+{
+    RL_GUARD(h);
+    (void)cudaGetLastError();
+    if (!h || !h->gv || round0 < 0 || nb < 1 || nb > h->gv->a.B || !out || !n_out)
+        return fail(RL_EINVAL, "rl_gvns_run_local: bad arguments");
+    CK(cudaSetDevice(h->device));
+    int rc = gv_launch_round(h, round0, round0 + nb, 2);
+    if (rc)
+        return rc;
+    GvnsArgs &a = h->gv->a;
+    int64_t scal[GV_FBCOST0];
+    CK(cudaMemcpyAsync(scal, a.scal, sizeof scal, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(out, a.rbest, (size_t)nb * 3 * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (scal[GV_ERROR])
+        return fail(RL_ECUDA, "gvns: more shake fallbacks in one round than slots (%d)",
+                    a.fb_slots);
+    *n_out = scal[GV_LOCAL_NB];
+    return 0;
+}
+
+// Copy the candidate of round jr of the last local batch to device memory
+// d_plan (2KT bytes: m rows then r rows).  Synchronous.
+extern "C" int rl_gvns_export(rl_instance *h, int jr, uint8_t *d_plan)
+{
+    RL_GUARD(h);
+    (void)cudaGetLastError();
+    if (!h || !h->gv || jr < 0 || jr >= h->gv->a.B || !d_plan)
+        return fail(RL_EINVAL, "rl_gvns_export: bad arguments");
+    CK(cudaSetDevice(h->device));
+    k_gvns_export<<<1, 1024, 0, h->stream>>>(h->gv->a, jr, d_plan);
+    CKL();
     CK(cudaStreamSynchronize(h->stream));
     return 0;
 }

@@ -133,7 +133,9 @@ def sharded_vnd(inst, plan, k_max=4, group=None, local_vnd=None, device="cpu",
 # ---------------------------------------------------------------- replicas
 
 class DeviceRounds:
-    """Round backend of ``sharded_gvns`` on this rank's GPU (gvns_impl.cuh)."""
+    """Round backend of ``sharded_gvns`` on this rank's GPU (gvns_impl.cuh):
+    speculative local batches (rl_gvns_run_local), the winning candidate's
+    export and the job winner's import."""
 
     def __init__(self, inst):
         import torch
@@ -144,15 +146,20 @@ class DeviceRounds:
         self.buf = torch.empty(2 * self.KT, dtype=torch.uint8, device="cuda")
         self.device = "cuda"
 
-    def begin(self, workers, worker_offset, config, sm, sr):
+    def begin(self, workers, worker_offset, config, sm, sr, batch=1):
         return self.dev.gvns_begin(workers, config.k_max, config.k_vnd_max, config.seed, sm, sr,
-                                   worker_offset=worker_offset)
+                                   worker_offset=worker_offset, batch=batch)
 
-    def round(self, round_index, strength):
+    def run_local(self, round0, strength, nb):
         self.dev.gvns_set_strength(strength)
-        self.dev.gvns_round(round_index, accept=False)
-        cost, w = self.dev.gvns_candidate(self.buf.data_ptr())
-        return cost, w, self.buf
+        return self.dev.gvns_run_local(round0, nb)
+
+    def export(self, jr):
+        self.dev.gvns_export(jr, self.buf.data_ptr())
+        return self.buf
+
+    def plan_buffer(self):
+        return self.buf
 
     def adopt(self, plan_tensor, cost):
         self.dev.gvns_import(plan_tensor.data_ptr(), cost)
@@ -162,16 +169,31 @@ class DeviceRounds:
         return sm, sr
 
 
-def sharded_gvns(inst, config, group=None, backend=None, start_plan=None):
+def _batch_rounds(local_workers):
+    """Rounds per speculative batch of a rank: enough worker slots (about
+    512) to fill its device, at most 4 (like gvns._batch)."""
+    return max(1, min(4, 512 // max(local_workers, 1)))
+
+
+def sharded_gvns(inst, config, group=None, backend=None, start_plan=None, batch=None):
     """GVNS whose W workers are split in contiguous blocks over the ranks
-    (BASELINE config 5: 1,024 replicas over 8 GPUs).  Every round each rank
-    runs its block, the job all-gathers the per-rank bests (cost, global
-    worker) and takes the minimum (lowest worker on ties, gvns.py:170-174),
-    the winning rank broadcasts its candidate plan, and every rank applies
-    the acceptance and strength step (gvns.py:207-215) identically.  The
-    wall-clock budget is decided on rank 0 and travels in the same
-    all-gather (one collective per round, plus the plan broadcast when the
-    incumbent improves).
+    (BASELINE config 5: 1,024 replicas over 8 GPUs), in speculative batches
+    of rounds with one collective per batch.
+
+    Each rank runs rounds r0 .. r0+nb-1 of its worker block at once, every
+    round shaking the current incumbent with the strength it has if the
+    rounds before it do not improve (round RNG streams depend only on (seed,
+    round, worker), gvns.py:88-90).  One all-gather carries every rank's
+    per-round best (cost, global worker) and rank 0's budget decision; all
+    ranks then walk the rounds in order, take each round's minimum (lowest
+    worker on ties, gvns.py:170-174) and stop at the first one that improves
+    the incumbent (gvns.py:207-215): its winner broadcasts the candidate and
+    every rank adopts it; the rounds after it are discarded and re-run from
+    the new incumbent by the next batch.  The trajectory is therefore the
+    sequential reference's, round for round.  The batch size adapts like
+    the single-GPU loop: 1 after an accepted round, doubled (up to ``batch``)
+    after a batch without one.  The wall-clock budget is checked between
+    batches (overshoot at most one batch).
     Returns the reference's GvnsResult on every rank."""
     import time
 
@@ -186,6 +208,8 @@ def sharded_gvns(inst, config, group=None, backend=None, start_plan=None):
     dev = getattr(be, "device", "cpu")
     W = config.workers
     w_lo, w_hi = shard_bounds(W, rank, world)
+    local = w_hi - w_lo
+    B = batch if batch is not None else _batch_rounds(-(-W // world))
     start = time.monotonic()
     if start_plan is None:
         if hasattr(be, "initial_solution"):
@@ -196,40 +220,55 @@ def sharded_gvns(inst, config, group=None, backend=None, start_plan=None):
             sm0, sr0 = p.setup_m, p.setup_r
     else:
         sm0, sr0 = start_plan.setup_m, start_plan.setup_r
-    local = w_hi - w_lo
-    inc_cost = be.begin(max(local, 1), w_lo, config, sm0, sr0)
-    strength, rounds = 1, 0
+    inc_cost = be.begin(max(local, 1), w_lo, config, sm0, sr0, batch=B)
+    strength, rounds, nb = 1, 0, 1
     BIG = (1 << 63) - 1
+    cap = config.max_rounds
 
-    def keep_going(done):   # rank 0's budget check before a round (gvns.py:197-199)
-        return not (time.monotonic() - start > config.t_max or (
-            config.max_rounds is not None and done >= config.max_rounds))
+    def keep_going(done):   # rank 0's budget check before a batch (gvns.py:197-199)
+        return not (time.monotonic() - start > config.t_max or (cap is not None and done >= cap))
 
     go = torch.tensor([1 if rank != 0 or keep_going(0) else 0], dtype=torch.int64, device=dev)
     dist.broadcast(go, src=0, group=group)
     going = int(go[0]) == 1
     while going:
-        cost, w, plan = be.round(rounds, strength)
-        if local == 0:
-            cost, w = BIG, BIG
-        # one all-gather per round: (cost, global worker) of every rank, and
-        # rank 0's budget decision for the next round rides along
-        nxt = 1 if rank != 0 or keep_going(rounds + 1) else 0
-        mine = torch.tensor([cost, w, nxt], dtype=torch.int64, device=dev)
-        allb = [torch.zeros(3, dtype=torch.int64, device=dev) for _ in range(world)]
+        want = nb if cap is None else max(1, min(nb, cap - rounds))
+        res = be.run_local(rounds, strength, want) if local else [(BIG, BIG)] * want
+        # one all-gather per batch: [valid rounds, go, (cost, worker) x want]
+        mine = torch.full((2 + 2 * want,), BIG, dtype=torch.int64)
+        mine[0] = len(res)
+        # rank 0's wall-clock decision for the next batch rides along
+        # (gvns.py:197-199; the round cap is checked by every rank below)
+        mine[1] = 1 if rank != 0 or time.monotonic() - start <= config.t_max else 0
+        for j, (c, w) in enumerate(res):
+            mine[2 + 2 * j] = c
+            mine[3 + 2 * j] = w
+        mine = mine.to(dev)
+        allb = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allb, mine, group=group)
         rows = [t.tolist() for t in allb]
-        going = int(rows[0][2]) == 1
-        pairs = [(int(r[0]), int(r[1])) for r in rows]
-        best_cost, best_w = min(pairs)
-        src = min(r for r in range(world) if pairs[r] == (best_cost, best_w))
-        improved = best_cost < inc_cost
-        if improved:
+        n_use = min(int(r[0]) for r in rows)
+        win = None
+        for j in range(n_use):
+            pairs = [(int(r[2 + 2 * j]), int(r[3 + 2 * j])) for r in rows]
+            best = min(pairs)
+            if best[0] < inc_cost:
+                win = (j, best, min(q for q in range(world) if pairs[q] == best))
+                break
+            strength = next_strength(strength, False, config.k_max)
+        if win is not None:
+            j, (best_cost, _), src = win
+            plan = be.export(j) if rank == src else be.plan_buffer()
             dist.broadcast(plan, src=src, group=group)
             be.adopt(plan, best_cost)
             inc_cost = best_cost
-        strength = next_strength(strength, improved, config.k_max)
-        rounds += 1
+            strength = next_strength(strength, True, config.k_max)
+            rounds += j + 1
+            nb = 1
+        else:
+            rounds += n_use
+            nb = 1 if n_use == 0 else min(2 * nb, B)
+        going = int(rows[0][1]) == 1 and (cap is None or rounds < cap)
     sm, sr = be.incumbent()
     return GvnsResult(SetupPlan(sm, sr), inc_cost, rounds, time.monotonic() - start,
                       rounds * W)

@@ -98,7 +98,7 @@ def test_shard_bounds_cover_products_in_order():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
 
 
-def _gvns_worker(rank, world, port, out_q):
+def _gvns_worker(rank, world, port, out_q, batch=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -115,7 +115,7 @@ def _gvns_worker(rank, world, port, out_q):
                             g.setup_cost_r, g.holding_cost_m, g.holding_cost_r,
                             g.unit_cost_m, g.unit_cost_r)
             cfg = SolverConfig(t_max=1e9, k_max=3, workers=3, seed=7, max_rounds=6)
-            r = sharded_gvns(inst, cfg, backend=OracleRounds(inst))
+            r = sharded_gvns(inst, cfg, backend=OracleRounds(inst), batch=batch)
             res.append((ci, r.cost, r.rounds, r.shake_calls, r.plan.setup_m.tobytes(),
                         r.plan.setup_r.tobytes()))
         out_q.put((rank, res))
@@ -123,15 +123,18 @@ def _gvns_worker(rank, world, port, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_replicas_equal_reference_gvns(world):
-    """Workers split over ranks (BASELINE config 5 shape): the cross-rank
-    best-of join reproduces the reference gvns() (W=3, 6 rounds) exactly."""
+@pytest.mark.parametrize("world,batch", [(2, None), (3, None), (2, 1), (3, 5)])
+def test_sharded_replicas_equal_reference_gvns(world, batch):
+    """Workers split over ranks (BASELINE config 5 shape), speculative
+    batches of rounds with one collective per batch: the cross-rank best-of
+    join reproduces the reference gvns() (W=3, 6 rounds) exactly, whatever
+    the batch size."""
     from conftest import golden
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gvns_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gvns_worker, args=(r, world, port, q, batch))
+             for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=600) for _ in procs)

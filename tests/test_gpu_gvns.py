@@ -155,10 +155,13 @@ def test_gvns_k1000_matches_reference():
         assert _plan_sha(res.plan) == g["plan_sha"], name
 
 
-def test_sharded_replicas_device_backend_single_rank():
-    """The replica-sharded driver on the device backend (candidate export,
-    NCCL all-gather/broadcast, import) reproduces the reference's K=1000
-    W=16 GVNS with one rank; multi-rank splits are covered on gloo."""
+@pytest.mark.parametrize("batch", [None, 1, 3])
+def test_sharded_replicas_device_backend_single_rank(batch):
+    """The replica-sharded driver on the device backend (local speculative
+    batches, candidate export, NCCL all-gather/broadcast, import) reproduces
+    the reference's K=1000 W=16 GVNS and the W=128 x 4 replica golden with
+    one rank, whatever the batch size; multi-rank splits are covered on
+    gloo."""
     import socket
 
     import torch
@@ -175,9 +178,15 @@ def test_sharded_replicas_device_backend_single_rank():
             g = json.load(f)["W16_R4"]
         inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
         cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=16, seed=0, max_rounds=4)
-        res = sharded_gvns(inst, cfg)
+        res = sharded_gvns(inst, cfg, batch=batch)
         assert res.cost == g["cost"] and res.rounds == 4 and res.shake_calls == 64
         assert _plan_sha(res.plan) == g["plan_sha"]
+        with open(os.path.join(GOLDEN, "gvns_c5.json")) as f:
+            g5 = json.load(f)["W128_R4"]
+        cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=128, seed=0, max_rounds=4)
+        res = sharded_gvns(inst, cfg, batch=batch)
+        assert res.cost == g5["cost"] and res.rounds == 4
+        assert _plan_sha(res.plan) == g5["plan_sha"]
     finally:
         dist.destroy_process_group()
 
