@@ -91,12 +91,17 @@ __device__ inline int64_t gv_strength(const GvnsArgs &g, int j)
     return k;
 }
 
-// The same test segment by segment over prefix sums cd[t] = sum_{i<t} D,
+// Feasibility of a shaken product's rows over prefix sums cd[t] = sum_{i<t} D,
 // cr[t] = sum_{i<t} R (closed form of DESIGN.md 3: x_R = min(seg, cr[u+1] -
-// X) at sR setups): one iteration per setup instead of per period.
+// X) at sR setups) with the whole warp (k_shake): lane l
+// owns periods [lL, lL + L); the cumulative remanufacturing X entering each
+// lane's periods comes from a warp scan of the (min, +)-affine maps X ->
+// min(X + seg, cr[u+1]) of its sR setups (as base_pass), then every lane
+// checks its own segments.  A few hundred cycles instead of one dependent
+// step per segment on lane 0.
 template <typename V>
-__device__ inline bool row_feasible_prefix(const V *cd, const V *cr, int T, const uint32_t *row,
-                                           int NW)
+__device__ inline bool warp_row_feasible(const V *cd, const V *cr, int T, const uint32_t *row,
+                                         int NW, int lane)
 {
     auto next_setup = [&](int x) {   // first setup >= x, T if none
         if (x >= T)
@@ -107,22 +112,40 @@ __device__ inline bool row_feasible_prefix(const V *cd, const V *cr, int T, cons
             bits = row[w] | row[NW + w];
         return bits ? min((w << 5) + __ffs(bits) - 1, T) : T;
     };
-    int u = next_setup(0);
-    if (cd[u] > 0)
-        return false;   // demand before the first setup (_kernels.py:58-60)
-    V X = 0;
-    while (u < T) {
-        const int v = next_setup(u + 1);
-        const V seg = cd[v] - cd[u];
-        const bool m = (row[u >> 5] >> (u & 31)) & 1u, r = (row[NW + (u >> 5)] >> (u & 31)) & 1u;
-        const V avail = cr[u + 1] - X;
-        const V xr = r ? (seg < avail ? seg : avail) : V(0);
-        if (seg - xr > 0 && !m)
-            return false;
-        X += xr;
-        u = v;
+    const int L = (T + 31) >> 5;
+    const int lo = min(lane * L, T), hi = min(lo + L, T);
+    const V INF = VInf<V>::value;
+    V A = 0, B = INF;
+    for (int u = lo; u < hi; ++u) {
+        if (!((row[NW + (u >> 5)] >> (u & 31)) & 1u))
+            continue;   // only remanufacturing setups move X
+        const V seg = cd[next_setup(u + 1)] - cd[u];
+        A += seg;
+        B = vmin<V>(B + seg, cr[u + 1]);
     }
-    return true;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const V a2 = __shfl_up_sync(FULL, A, off), b2 = __shfl_up_sync(FULL, B, off);
+        if (lane >= off) {
+            B = vmin<V>(b2 + A, B);
+            A = a2 + A;
+        }
+    }
+    const V pa = __shfl_up_sync(FULL, A, 1), pb = __shfl_up_sync(FULL, B, 1);
+    V X = lane == 0 ? V(0) : vmin<V>(pa, pb);
+    bool ok = true;
+    for (int u = lo; u < hi; ++u) {
+        const bool m = (row[u >> 5] >> (u & 31)) & 1u, r = (row[NW + (u >> 5)] >> (u & 31)) & 1u;
+        if (!(m | r))
+            continue;
+        const V seg = cd[next_setup(u + 1)] - cd[u];
+        const V xr = r ? vmin<V>(seg, cr[u + 1] - X) : V(0);
+        ok &= !(seg - xr > 0 && !m);
+        X += xr;
+    }
+    if (lane == 0)
+        ok &= cd[next_setup(0)] <= 0;   // demand before the first setup (_kernels.py:58-60)
+    return __all_sync(FULL, ok);
 }
 
 // Feasibility of one product's rows under row_cost (_kernels.py:58-82):
@@ -372,18 +395,21 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
                     ++j;
                 tw[(int64_t)j * 2 * NW + mat * NW + (t >> 5)] ^= 1u << (t & 31);
             }
-            for (int j = 0; j < n && ok; ++j) {
-                const uint32_t *row = tw + (int64_t)j * 2 * NW;
-                const int64_t k = tp[j];
-                if (drow) {
-                    const V *cd = drow + (int64_t)j * 2 * (T + 1);
-                    ok = row_feasible_prefix<V>(cd, cd + T + 1, T, row, NW);
-                    continue;
+            if (!drow)
+                for (int j = 0; j < n && ok; ++j) {
+                    const uint32_t *row = tw + (int64_t)j * 2 * NW;
+                    const int64_t k = tp[j];
+                    const V *dd = in.dem + k * T, *rr = in.ret + k * T;
+                    ok = row_feasible<V>(dd, rr, T,
+                                         [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
+                                         [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
                 }
-                const V *dd = in.dem + k * T, *rr = in.ret + k * T;
-                ok = row_feasible<V>(dd, rr, T,
-                                     [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
-                                     [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
+        }
+        if (drow) {   // touched rows and their prefix sums in shared memory: warp test
+            __syncwarp();
+            for (int j = 0; j < n && ok; ++j) {
+                const V *cd = drow + (int64_t)j * 2 * (T + 1);
+                ok = warp_row_feasible<V>(cd, cd + T + 1, T, tw + (int64_t)j * 2 * NW, NW, lane);
             }
         }
         ok = __shfl_sync(FULL, (int)ok, 0);
