@@ -333,8 +333,12 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
         }
         n = __shfl_sync(FULL, n, 0);
         __syncwarp();
-        // rows of the touched products: incumbent bits by ballot, then flips
-        for (int j = 0; j < n; ++j) {
+        // rows of the touched products, product by product: incumbent bits
+        // by ballot, the flips that fall on the product (_flip_flat,
+        // gvns.py:93-98), prefix sums, the warp feasibility test; an
+        // infeasible product ends the attempt (most redraws fail early)
+        bool ok = true;
+        for (int j = 0; j < n && ok; ++j) {
             const int64_t k = tp[j];
             const uint8_t *im = g.inc + k * T, *ir = g.inc + g.KT + k * T;
             uint32_t *row = tw + (int64_t)j * 2 * NW;
@@ -347,7 +351,16 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
                     row[NW + (base >> 5)] = wr;
                 }
             }
-            if (drow) {   // prefix sums of the rows for lane 0's segment walk
+            if (lane == 0)
+                for (int64_t i = 0; i < k_eff; ++i) {
+                    const int64_t p = P[i];
+                    const int64_t rem = p % g.KT;
+                    if (rem / T != k)
+                        continue;
+                    const int t = (int)(rem % T);
+                    row[(p < g.KT ? 0 : NW) + (t >> 5)] ^= 1u << (t & 31);
+                }
+            if (drow) {   // prefix sums of the rows, then the warp test
                 V *cd = drow + (int64_t)j * 2 * (T + 1), *cr = cd + T + 1;
                 V cdc = 0, crc = 0;
                 if (lane == 0) {
@@ -375,41 +388,21 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
                     cdc = __shfl_sync(FULL, d, 31);
                     crc = __shfl_sync(FULL, r, 31);
                 }
+                __syncwarp();
+                ok = warp_row_feasible<V>(cd, cr, T, row, NW, lane);
             } else {
                 for (int t = lane; t < T; t += 32) {   // warm L1 for lane 0's walk
                     (void)__ldg(in.dem + k * T + t);
                     (void)__ldg(in.ret + k * T + t);
                 }
-            }
-        }
-        __syncwarp();
-        bool ok = true;
-        if (lane == 0) {
-            for (int64_t i = 0; i < k_eff; ++i) {   // _flip_flat (gvns.py:93-98)
-                const int64_t p = P[i];
-                const int mat = p < g.KT ? 0 : 1;
-                const int64_t rem = p % g.KT, k = rem / T;
-                const int t = (int)(rem % T);
-                int j = 0;
-                while (tp[j] != k)
-                    ++j;
-                tw[(int64_t)j * 2 * NW + mat * NW + (t >> 5)] ^= 1u << (t & 31);
-            }
-            if (!drow)
-                for (int j = 0; j < n && ok; ++j) {
-                    const uint32_t *row = tw + (int64_t)j * 2 * NW;
-                    const int64_t k = tp[j];
+                __syncwarp();
+                if (lane == 0) {
                     const V *dd = in.dem + k * T, *rr = in.ret + k * T;
                     ok = row_feasible<V>(dd, rr, T,
                                          [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
                                          [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
                 }
-        }
-        if (drow) {   // touched rows and their prefix sums in shared memory: warp test
-            __syncwarp();
-            for (int j = 0; j < n && ok; ++j) {
-                const V *cd = drow + (int64_t)j * 2 * (T + 1);
-                ok = warp_row_feasible<V>(cd, cd + T + 1, T, tw + (int64_t)j * 2 * NW, NW, lane);
+                ok = __shfl_sync(FULL, (int)ok, 0);
             }
         }
         ok = __shfl_sync(FULL, (int)ok, 0);
