@@ -71,7 +71,9 @@ int rl_oracle_optimal(rl_instance *h, int64_t *cost, uint8_t *sm, uint8_t *sr);
  * Bit 4: int64 values and int64 costs whatever the range proof allows (the
  * general path; the narrow exact widths are the default).
  * Bit 5: reserved (lane kernel off, the default).  Bit 6: T <= 63 runs the
- * lane-per-product kernel (k_vnd_lane; exact, slower at C3: DESIGN.md 5). */
+ * lane-per-product kernel (k_vnd_lane; exact, slower at C3: DESIGN.md 5).
+ * Bit 7: never the 16-bit long-horizon rows.  Bit 8: T > 63 always one CTA
+ * per product (measured slower at C4: 203 vs 137 ms). */
 int rl_instance_set_variant(rl_instance *h, int variant);
 /* info[0..5] = K, T, bytes per period value (4|8), bytes per cost (4|8),
  * SM count, warps per CTA of the resident VND kernel. */

@@ -802,6 +802,7 @@ struct rl_instance {
     double sdr_max = 0.0;                  // max over products of sum D + sum R
     bool p16 = false;                      // every product's sum D, sum R < 2^16
     bool no16 = false;                     // variant bit 7: never the 16-bit rows (A/B)
+    bool cta_always = false;               // variant bit 8: CTA per product for T > 63 (A/B)
 };
 
 struct GvnsState;
@@ -1071,11 +1072,12 @@ extern "C" int rl_instance_set_variant(rl_instance *h, int variant)
 {
     RL_GUARD(h);
     // bit 0 (two products per warp) was removed: measured slower
-    if (!h || variant < 0 || variant > 255 || (variant & 12) == 12 || (variant & 1) ||
+    if (!h || variant < 0 || variant > 511 || (variant & 12) == 12 || (variant & 1) ||
         (variant & 96) == 96)
         return fail(RL_EINVAL, "rl_instance_set_variant: bad arguments");
     h->lane_mode = (variant & 32) ? 1 : (variant & 64) ? 2 : 0;
     h->no16 = (variant & 128) != 0;
+    h->cta_always = (variant & 256) != 0;
     h->cta_long = (variant & 2) == 0;
     h->skip_mode = (variant & 4) ? 1 : (variant & 8) ? 2 : 0;
     const bool f64 = (variant & 16) != 0;
@@ -1317,7 +1319,7 @@ static int launch_vnd_range(rl_instance *h, int k_max, const uint8_t *sm_in, con
     // at C4 scale one warp per product keeps 2.4x more products in flight
     // and measured 296 ms vs 434 ms
     const bool cta = std::is_same<Mask, MaskSmem>::value && h->cta_long &&
-                     nprod <= (int64_t)h->sms * 2;
+                     (nprod <= (int64_t)h->sms * 2 || h->cta_always);
     // skip pays when the launch is latency-bound: fewer products than ~2
     // waves of resident warps (C2, GVNS) -- measured, DESIGN.md section 5
     const bool skip = std::is_same<Mask, MaskReg>::value &&
