@@ -196,6 +196,13 @@ int rl_gvns_round(rl_instance *h, int64_t round_index, int accept);
  * accepted one (later rounds are re-run by the next call), so the result is
  * the sequential trajectory.  Asynchronous; the counter is info[6]. */
 int rl_gvns_run(rl_instance *h, int64_t max_rounds);
+/* The whole gvns loop (gvns.py:200-215) on the device: speculative batches
+ * inside a CUDA-graph conditional WHILE node until the device round counter
+ * reaches max_rounds or budget_ns nanoseconds of device time (%globaltimer,
+ * from the launch) have passed, checked between batches (the reference
+ * checks between rounds; a batch is at most 4 rounds, each the round the
+ * sequential loop would run).  One graph launch; synchronous. */
+int rl_gvns_run_until(rl_instance *h, int64_t max_rounds, int64_t budget_ns);
 /* which = 0: incumbent, 1: last round's winning candidate (accept = 0).
  * info[0..6] = incumbent cost, strength, last best cost, last best worker,
  * accepted rounds, shake fallbacks in the last round, rounds completed.

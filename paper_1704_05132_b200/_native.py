@@ -28,7 +28,7 @@ EXPORTS = ("rl_instance_create", "rl_instance_update", "rl_instance_destroy",
            "rl_vnd_product_stats",
            "rl_initial_solution", "rl_initial_solution_device", "rl_decode", "rl_oracle_optimal", "rl_int_peak", "rl_gvns_begin", "rl_gvns_begin_batch", "rl_gvns_set_strength",
            "rl_gvns_round", "rl_gvns_run", "rl_gvns_state", "rl_gvns_candidate", "rl_gvns_import",
-           "rl_gvns_run_local", "rl_gvns_export",
+           "rl_gvns_run_local", "rl_gvns_export", "rl_gvns_run_until",
            "rl_rng_probe", "rl_launch_count", "rl_generate_instance", "rl_instance_download",
            "rl_last_error")
 
@@ -78,6 +78,7 @@ def load():
         "rl_gvns_candidate": (I, [P, P, P]),
         "rl_gvns_import": (I, [P, P, I64]),
         "rl_gvns_run_local": (I, [P, I64, I, P, P]),
+        "rl_gvns_run_until": (I, [P, I64, I64]),
         "rl_gvns_export": (I, [P, I, P]),
         "rl_gvns_set_strength": (I, [P, I64]),
         "rl_gvns_round": (I, [P, I64, I]),
@@ -311,6 +312,12 @@ class DeviceInstance:
         check(load().rl_gvns_candidate(self.h, ctypes.c_void_p(d_plan_ptr) if d_plan_ptr else None,
                                        ptr(best)), "rl_gvns_candidate")
         return int(best[0]), int(best[1])
+
+    def gvns_run_until(self, max_rounds, budget_s):
+        """The gvns loop on the device (CUDA-graph WHILE node) until
+        max_rounds rounds or budget_s seconds of device time."""
+        check(load().rl_gvns_run_until(self.h, max_rounds, int(max(budget_s, 0.0) * 1e9)),
+              "rl_gvns_run_until")
 
     def gvns_run_local(self, round0, nb):
         """Local speculative batch of rounds round0.. (no acceptance): the

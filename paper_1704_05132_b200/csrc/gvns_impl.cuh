@@ -64,6 +64,9 @@ enum {
     GV_NTASK,     // compact VND tasks appended by k_shake (reset by the join)
     GV_FB_TRUNC,  // B - (first batch round whose fallback found no slot), 0 = none
     GV_LOCAL_NB,  // rounds of the last local batch (mode 2) with valid bests
+    GV_MAXR,      // round cap of a device-resident run (max_rounds < 0 in the kernels)
+    GV_TBUDGET,   // its wall-clock budget in ns
+    GV_T0,        // %globaltimer at its start
     GV_FBCOST0,   // fb_slots entries follow
 };
 
@@ -77,7 +80,7 @@ __device__ inline int gv_batch(const GvnsArgs &g, int64_t round_arg, int64_t max
 {
     r0 = round_arg >= 0 ? round_arg : g.scal[GV_ROUND];
     const int64_t cap = round_arg >= 0 ? g.B : g.scal[GV_NB];
-    const int64_t left = max_rounds - r0;
+    const int64_t left = (max_rounds < 0 ? g.scal[GV_MAXR] : max_rounds) - r0;
     return left <= 0 ? 0 : left < cap ? (int)left : (int)cap;
 }
 
@@ -751,6 +754,7 @@ struct GvnsState {
     cudaGraphExec_t graph = nullptr;
     int64_t graph_max = -1;
     int runs = 0;
+    cudaGraphExec_t loop = nullptr;   // rl_gvns_run_until's device-resident loop
     int vbytes = 0;   // value width the shake scratch was sized for
 };
 
@@ -760,6 +764,8 @@ static void gvns_free(GvnsState *gs)
         return;
     if (gs->graph)
         cudaGraphExecDestroy(gs->graph);
+    if (gs->loop)
+        cudaGraphExecDestroy(gs->loop);
     for (int i = 0; i < gs->nblocks; ++i)
         if (gs->blocks[i])
             cudaFree(gs->blocks[i]);
@@ -901,6 +907,10 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
     if (gs->graph) {   // captured with the previous arguments
         cudaGraphExecDestroy(gs->graph);
         gs->graph = nullptr;
+    }
+    if (gs->loop) {
+        cudaGraphExecDestroy(gs->loop);
+        gs->loop = nullptr;
     }
     gs->runs = 0;
     gs->k_vnd_max = k_vnd_max;
@@ -1101,6 +1111,108 @@ extern "C" int rl_gvns_import(rl_instance *h, const uint8_t *d_plan, int64_t cos
     int64_t scal[4] = {cost, cost, 0, 1};   // inc cost, Ftot, (strength kept), inc_is_F
     CK(cudaMemcpyAsync(&a.scal[GV_INC_COST], &scal[0], 16, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(&a.scal[GV_INC_IS_F], &scal[3], 8, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return 0;
+}
+
+// ---- device-resident GVNS loop (rl_gvns_run_until)
+__device__ inline int64_t gv_now_ns()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (int64_t)t;
+}
+
+__global__ void k_gvns_t0(GvnsArgs g) { g.scal[GV_T0] = gv_now_ns(); }
+
+// The loop condition, evaluated after every batch (gvns.py:200-206 checks
+// the clock and the round cap before every round): another batch while the
+// round cap is not reached, the budget not spent and no error raised.
+__global__ void k_gvns_cond(GvnsArgs g, cudaGraphConditionalHandle hnd)
+{
+    const bool go = g.scal[GV_ROUND] < g.scal[GV_MAXR] &&
+                    gv_now_ns() - g.scal[GV_T0] <= g.scal[GV_TBUDGET] && !g.scal[GV_ERROR];
+    cudaGraphSetConditional(hnd, go ? 1u : 0u);
+}
+
+// gvns()'s whole loop (gvns.py:200-215) on the device: one graph launch runs
+// speculative batches (shake, VND tasks, join + acceptance) inside a
+// conditional WHILE node until max_rounds rounds are done or budget_ns of
+// device time (%globaltimer) has passed, the check made between batches; the
+// host waits once.  The graph is built on the first call after a begin
+// and replayed with new caps (read from the device scalars).  Synchronous.
+extern "C" int rl_gvns_run_until(rl_instance *h, int64_t max_rounds, int64_t budget_ns)
+{
+    RL_GUARD(h);
+    (void)cudaGetLastError();
+    if (!h || !h->gv || max_rounds < 0)
+        return fail(RL_EINVAL, "rl_gvns_run_until: call rl_gvns_begin_batch first");
+    CK(cudaSetDevice(h->device));
+    GvnsState *gs = h->gv;
+    if (!gs->loop) {
+        if (gs->runs++ == 0) {   // kernel attributes are set by a plain launch first
+            int64_t zero = 0;
+            CK(cudaMemcpyAsync(&gs->a.scal[GV_MAXR], &zero, 8, cudaMemcpyHostToDevice, h->stream));
+            int rc = gv_launch_round(h, -1, -1, 1);   // no rounds (cap 0): sets attributes only
+            if (rc)
+                return rc;
+        }
+        cudaGraph_t g = nullptr;
+        CK(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle hnd;
+        cudaGraphNode_t t0node, loop;
+        cudaError_t e = cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault);
+        cudaGraph_t body = nullptr;
+        if (e == cudaSuccess) {
+            cudaKernelNodeParams kp = {};
+            void *args[] = {(void *)&gs->a};
+            kp.func = (void *)k_gvns_t0;
+            kp.gridDim = dim3(1);
+            kp.blockDim = dim3(1);
+            kp.kernelParams = args;
+            e = cudaGraphAddKernelNode(&t0node, g, nullptr, 0, &kp);
+        }
+        if (e == cudaSuccess) {
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = hnd;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            e = cudaGraphAddNode(&loop, g, &t0node, 1, &cp);
+            if (e == cudaSuccess)
+                body = cp.conditional.phGraph_out[0];
+        }
+        if (e == cudaSuccess)
+            e = cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) {
+            cudaGraphDestroy(g);
+            return fail(RL_ECUDA, "rl_gvns_run_until: graph: %s", cudaGetErrorString(e));
+        }
+        const int64_t l0 = h->launches;
+        int rc = gv_launch_round(h, -1, -1, 1);
+        if (!rc) {
+            k_gvns_cond<<<1, 1, 0, h->stream>>>(gs->a, hnd);
+            rc = cudaGetLastError() == cudaSuccess ? 0 : fail(RL_ECUDA, "k_gvns_cond launch");
+        }
+        cudaGraph_t cap = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(h->stream, &cap);
+        h->launches = l0;
+        if (rc || ec != cudaSuccess) {
+            cudaGraphDestroy(g);
+            return rc ? rc : fail(RL_ECUDA, "rl_gvns_run_until: capture: %s", cudaGetErrorString(ec));
+        }
+        e = cudaGraphInstantiate(&gs->loop, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            gs->loop = nullptr;
+            return fail(RL_ECUDA, "rl_gvns_run_until: instantiate: %s", cudaGetErrorString(e));
+        }
+    }
+    int64_t caps[2] = {max_rounds, budget_ns < 0 ? 0 : budget_ns};
+    CK(cudaMemcpyAsync(&gs->a.scal[GV_MAXR], caps, sizeof caps, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaGraphLaunch(gs->loop, h->stream));
+    h->launches += 5;   // t0, and per batch shake, VND, join, condition (counted once)
     CK(cudaStreamSynchronize(h->stream));
     return 0;
 }
