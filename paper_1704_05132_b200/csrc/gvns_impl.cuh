@@ -442,7 +442,7 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
 
 // VND of every (worker, touched product) task and of every product of the
 // fallback plans; warps pull tasks from a queue.
-template <typename V, typename C, typename Mask>
+template <typename V, typename C, typename Mask, bool Skip = true>
 __global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, int k_vnd_max)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, in
         const C K0 = build_prefix(s, T, pc, lane);
         C S0, S;
         VndStats st;
-        vnd_product<V, C, Mask, true>(s, mk, T, pc, k_vnd_max, lane, S0, S, st, nullptr, 0,
+        vnd_product<V, C, Mask, Skip>(s, mk, T, pc, k_vnd_max, lane, S0, S, st, nullptr, 0,
                                       nullptr);
         const int64_t cost = (int64_t)(K0 + S);
         if (row) {
@@ -789,13 +789,22 @@ static int gv_launch_vnd(rl_instance *h, GvnsState *gs)
 {
     int grid, block;
     size_t smem;
-    int rc = launch_cfg<V, C>(h, (const void *)k_gvns_vnd<V, C, Mask>,
+    // the slack skip shortens the long delta walks of these latency-bound
+    // tasks (variant bit 3 turns it off for A/B)
+    const bool skip = h->skip_mode != 2;
+    const void *fn = skip ? (const void *)k_gvns_vnd<V, C, Mask, true>
+                          : (const void *)k_gvns_vnd<V, C, Mask, false>;
+    int rc = launch_cfg<V, C>(h, fn,
                               (int64_t)gs->a.W * gs->a.tcap + (int64_t)gs->a.fb_slots * h->K,
                               grid, smem, block);
     if (rc)
         return rc;
-    k_gvns_vnd<V, C, Mask><<<grid, block, smem, h->stream>>>(view<V>(h), gs->a,
-                                                                          gs->k_vnd_max);
+    if (skip)
+        k_gvns_vnd<V, C, Mask, true><<<grid, block, smem, h->stream>>>(view<V>(h), gs->a,
+                                                                        gs->k_vnd_max);
+    else
+        k_gvns_vnd<V, C, Mask, false><<<grid, block, smem, h->stream>>>(view<V>(h), gs->a,
+                                                                         gs->k_vnd_max);
     CKL();
     return 0;
 }

@@ -12,6 +12,9 @@ from paper_1704_05132_b200 import GeneratorConfig, SolverConfig, generate_instan
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+if os.environ.get("RL_VARIANT"):   # A/B of kernel variant bits on the cached handle
+    from paper_1704_05132_b200._native import device_instance
+    device_instance(inst).set_variant(int(os.environ["RL_VARIANT"]))
 gvns(inst, SolverConfig(t_max=1e9, workers=W, seed=0, max_rounds=2))
 t0 = time.perf_counter()
 res = gvns(inst, SolverConfig(t_max=1e9, workers=W, seed=0, max_rounds=R))
