@@ -1231,6 +1231,7 @@ extern "C" int rl_gvns_run_until(rl_instance *h, int64_t max_rounds, int64_t bud
 __global__ void k_gvns_export(GvnsArgs g, int jr, uint8_t *dst)
 {
     const int w = (int)g.rbest[3 * jr + 2];
+    RL_ASSERT(w >= 0 && w < g.W && (!g.fb[w] || g.fbslot[w] < g.fb_slots));
     const int tid = threadIdx.x;
     const int64_t KT2 = 2 * g.KT;
     if (g.fb[w]) {

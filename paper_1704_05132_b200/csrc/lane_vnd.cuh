@@ -77,6 +77,7 @@ struct LaneRows<V, C, true> {
     }
     __device__ void set_d(int t, V cd, V cr) const
     {
+        RL_ASSERT(cd >= 0 && cd < 32768 && cr >= 0 && cr < 32768);   // the 15-bit proof
         dr[t * 32] = (uint32_t)cd | (uint32_t)cr << 16;
     }
     __device__ XC<V, C> x(int t) const
@@ -384,7 +385,9 @@ __global__ void __launch_bounds__(32) k_vnd_lane(InstView<V> in, const uint8_t *
         __syncwarp();
         if (state == LN_WALK) {
             // one segment [u, v) of the walk (vnd_device.cuh walk_moves)
+            RL_ASSERT(u >= 0 && u < T);
             const int v = (u + 1) + __clzll((long long)(pSR << (u + 1)));
+            RL_ASSERT(v > u && v <= T);
             const bool mu = (pM >> u) & 1, ru = (pR >> u) & 1;
             const DR<V> ev = L.d(v);
             C c;

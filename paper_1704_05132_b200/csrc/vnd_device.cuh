@@ -150,8 +150,16 @@ struct DRStore<V, 2> {
         const uint32_t w = p[i];
         return DR<V>{V(w & 0xffffu), V(w >> 16)};
     }
-    __device__ void set_d(int i, V v) const { ((uint16_t *)p)[2 * i] = (uint16_t)v; }
-    __device__ void set_r(int i, V v) const { ((uint16_t *)p)[2 * i + 1] = (uint16_t)v; }
+    __device__ void set_d(int i, V v) const
+    {
+        RL_ASSERT(v >= 0 && v < 65536);   // the upload's 16-bit proof
+        ((uint16_t *)p)[2 * i] = (uint16_t)v;
+    }
+    __device__ void set_r(int i, V v) const
+    {
+        RL_ASSERT(v >= 0 && v < 65536);
+        ((uint16_t *)p)[2 * i + 1] = (uint16_t)v;
+    }
 };
 
 // {cpre, xin} with a 16-bit xin (SB = 2; xin <= sum R < 2^16)
@@ -177,6 +185,7 @@ struct XCStore16 {
     }
     __device__ void set(int i, V xv, C cv) const
     {
+        RL_ASSERT(xv >= 0 && xv < 65536);
         x[i] = (uint16_t)xv;
         c[i] = cv;
     }

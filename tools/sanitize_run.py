@@ -12,7 +12,7 @@ from paper_1704_05132_b200._native import DeviceInstance  # noqa: E402
 for K, T in ((40, 52), (6, 130), (3, 5)):
     inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=1))
     start = initial_solution(inst)
-    for variant in (0, 2, 4, 8):
+    for variant in (0, 2, 4, 8, 16, 64, 128, 256):
         dev = DeviceInstance(inst)
         dev.set_variant(variant)
         dev.vnd(start.setup_m, start.setup_r)
