@@ -1141,7 +1141,9 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
     const unsigned lt = (1u << lane) - 1;
     constexpr bool kSkip = Skip && std::is_same<Mask, MaskReg>::value;
     constexpr bool kRegMask = std::is_same<Mask, MaskReg>::value;
-    typename PatchOf<Mask>::type pw{};
+    // the base rows (a valid candidate for the discarded steps of idle lanes)
+    typename PatchOf<Mask>::type pw =
+        PatchOf<Mask>::make(mk, 0, 0, mk.m(0), mk.r(0), mk.m(0), mk.r(0));
     int u = 0, b = 0, slot = 0, tu = 0;   // tu: kind (m | r << 1) of setup u
     V X = 0, cdu = 0, cru = 0;
     C acc = 0;
@@ -1194,13 +1196,22 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
                 }
             }
         }
-        if (state == 2) {
-#ifdef RL_WALK_STATS
-            ++ws_cur;
-            ++ws_lane;
+#ifndef RL_STEP_BRANCH
+#define RL_STEP_BRANCH 0
 #endif
-            // one segment of the walk, branch-free (every busy lane issues the
-            // same instructions): cost, resync test, finish, argmin update
+        // one segment of the walk, branch-free (every busy lane issues the
+        // same instructions): cost, resync test, finish, argmin update.
+        // Issued unconditionally (no divergent branch and reconvergence per
+        // iteration): idle lanes step from period T - 1 (a valid query whose
+        // next setup is the end, T) and their results are discarded.
+        const bool walking = state == 2;
+        if (RL_STEP_BRANCH == 0 || walking) {
+#ifdef RL_WALK_STATS
+            ws_cur += walking;
+            ws_lane += walking;
+#endif
+            if (!walking)
+                u = T - 1;   // a valid start for the discarded step
             // register masks test the candidate's bits directly (measured
             // faster); shared-memory masks carry the kind from the nx table
             int tv = 0, v;
@@ -1257,10 +1268,10 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
             // total = acc + S - cpre[v]: the base suffix when resynced, and
             // just acc at v = T (xc[T].c = S); only read when fin
             const bool fin = v >= T || sync;
-            const bool take = ok && fin && total < best;
+            const bool take = walking && ok && fin && total < best;
             best = take ? total : best;
             key = take ? slot : key;
-            state = ok && !fin ? 2 : 0;
+            state = walking && ok && !fin ? 2 : 0;
         }
         const unsigned m = __ballot_sync(FULL, state == 0);
         const bool more = m != FULL || next * nw + wi < n;
