@@ -278,8 +278,11 @@ def issue_roofline(workload, kernel_ms, clocks, sms):
             "peak": peak / 1e9, "unit": "Gwarp-inst/s", "frac": achieved / peak,
             "peak_source": f"{sms} SMs x 4 schedulers x {mhz:.0f} MHz (SM clock under load)",
             "warp_inst_per_launch": ncu["warp_inst"], "kernel_ms": kernel_ms,
-            "lane_efficiency": (lanes / 32.0) if lanes else None,
-            "lane_slot_frac": (achieved / peak) * (lanes / 32.0) if lanes else None,
+            "threads_per_inst_frac": (lanes / 32.0) if lanes else None,
+            "threads_note": "not-predicated threads per issued instruction / 32 (ncu); since "
+                            "round 2 the walk step is issued unconditionally, so this counts "
+                            "idle lanes issuing the discarded step -- the walk's useful-lane "
+                            "share is ~0.46 at C3 (tools/walk_stats.py, DESIGN.md 5)",
             "traffic": traffic_bytes(workload), "ncu": ncu}
 
 
