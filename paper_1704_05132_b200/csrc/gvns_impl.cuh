@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(128) k_gvns_vnd(InstView<V> in, GvnsArgs g, in
             plan = g.fbplan + (int64_t)slot * 2 * g.KT;
         }
         stage_begin(s, in, k, lane);
-        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k, in.T);
+        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k, in.T, in.one);
         Mask mk;
         if (row) {
             // words -> plan bytes layout for load_rows: go through the slot's mv buffer

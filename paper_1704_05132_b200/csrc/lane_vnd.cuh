@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(32) k_vnd_lane(InstView<V> in, const uint8_t *
         o.moves[k] = moves;
     };
     auto load_product = [&]() {
-        pc = load_costs<C>(in.cost6, in.K, k, T);
+        pc = load_costs<C>(in.cost6, in.K, k, T, in.one);
         const V *d = in.dem + k * T, *r = in.ret + k * T;
         const uint8_t *a = sm_in + k * T, *bb = sr_in + k * T;
         V cd = 0, cr = 0;

@@ -76,10 +76,12 @@ struct InstView {
     int T;
     const V *dem, *ret;
     const int64_t *cost6;   // 6 x K int64
+    int one;                // 1, a kernel parameter the compiler cannot see through
 };
 
 template <typename C>
-__device__ inline ProductCosts<C> load_costs(const int64_t *c6, int64_t K, int64_t k, int T)
+__device__ inline ProductCosts<C> load_costs(const int64_t *c6, int64_t K, int64_t k, int T,
+                                             int one)
 {
     ProductCosts<C> p;
     p.km = C(c6[k]);
@@ -90,6 +92,8 @@ __device__ inline ProductCosts<C> load_costs(const int64_t *c6, int64_t K, int64
     p.pr = C(c6[5 * K + k]);
     p.a0 = p.pm + C(T) * p.hm;            // wrapping is exact
     p.b0 = p.pr - p.pm - C(T) * p.hr;
+    p.one = C(one);                        // 1, opaque to the compiler (kernel parameter)
+    p.mone = -p.one;
     return p;
 }
 
@@ -187,7 +191,7 @@ __device__ inline C load_product(const Slot<V, C, SB> &s, const InstView<V> &in,
                                  ProductCosts<C> &pc, Mask &mk)
 {
     stage_begin(s, in, k, lane);
-    pc = load_costs<C>(in.cost6, in.K, k, in.T);
+    pc = load_costs<C>(in.cost6, in.K, k, in.T, in.one);
     mk = load_rows(s, Mask{}, sm, sr, k, in.T, lane);
     stage_end(s, in, k, lane, phase);
     return build_prefix(s, in.T, pc, lane);
@@ -400,7 +404,7 @@ __global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask, SB)) k_vnd(Ins
         // the stage aliases xc (free between products): no prefetch; the
         // copy's latency is hidden by the other resident warps
         stage_begin(s, in, k, lane);
-        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k, in.T);
+        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k, in.T, in.one);
         Mask mk = load_rows(s, Mask{}, sm_in, sr_in, k, T, lane);
         stage_end(s, in, k, lane, phase);
         const C K0 = build_prefix(s, T, pc, lane);
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
     uint32_t phase = 0;
     while (sh_k < o.k_hi) {
         const int64_t k = sh_k;
-        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k, in.T);
+        const ProductCosts<C> pc = load_costs<C>(in.cost6, in.K, k, in.T, in.one);
         C K0 = 0;
         if (warp == 0) {
             stage_begin(s, in, k, lane);   // stage aliases xc: no prefetch
@@ -1112,6 +1116,7 @@ static InstView<V> view(rl_instance *h)
     v.dem = (const V *)h->dem;
     v.ret = (const V *)h->ret;
     v.cost6 = h->cost6;
+    v.one = 1;
     return v;
 }
 

@@ -67,6 +67,10 @@ template <> struct VInf<int64_t> { static constexpr int64_t value = (int64_t)1 <
 template <typename C>
 struct ProductCosts {
     C km, kr, hm, hr, pm, pr, a0, b0;
+    // 1 and -1 the compiler cannot see through (derived from the horizon):
+    // x * one + y issues as an IMAD on the FMA pipe instead of an IADD3 on
+    // the ALU pipe, which bounds the int32 walk (ncu: ALU 83%, FMA 21%)
+    C one, mone;
 };
 
 template <typename V>
@@ -591,9 +595,17 @@ __device__ inline bool seg_cost(V cdu, V cru, V cdv, int u, bool m, bool r, V X,
     const V avail = cru - X;
     xr = r ? vmin(seg, avail) : V(0);
     const V xm = seg - xr;
-    // computed unconditionally (no branch): callers discard c when infeasible
-    c = (xr > 0 ? pc.kr : C(0)) + (xm > 0 ? pc.km : C(0)) + C(seg) * (pc.a0 - C(u) * pc.hm) +
-        C(xr) * (pc.b0 + C(u) * pc.hr);
+    // computed unconditionally (no branch): callers discard c when infeasible;
+    // a chain of multiply-adds (FMA pipe) rather than a three-input add
+    if constexpr (sizeof(C) == 4) {
+        C acc = xr > 0 ? pc.kr : C(0);
+        acc = C(seg) * (pc.a0 - C(u) * pc.hm) + acc;
+        acc = C(xr) * (pc.b0 + C(u) * pc.hr) + acc;
+        c = (xm > 0 ? pc.km : C(0)) * pc.one + acc;
+    } else {
+        c = (xr > 0 ? pc.kr : C(0)) + (xm > 0 ? pc.km : C(0)) +
+            C(seg) * (pc.a0 - C(u) * pc.hm) + C(xr) * (pc.b0 + C(u) * pc.hr);
+    }
     return !(xm > 0 && !m);
 }
 
@@ -1259,7 +1271,10 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
                 cru = eq.r;
             } else {
                 sync = past && X == bv.x;
-                total = acc + (S - bv.c);
+                if constexpr (sizeof(C) == 4)
+                    total = acc * pc.one + (bv.c * pc.mone + S);   // two IMADs, not an IADD3
+                else
+                    total = acc + (S - bv.c);
                 u = v;
                 tu = tv;
                 cdu = ev.d;
