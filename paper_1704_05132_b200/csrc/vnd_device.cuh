@@ -1245,10 +1245,10 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
             acc += c;
             X += xr;
             // past the move the rows equal the base plan's; only X may differ
-            const bool past = v < T && v > b;
-            bool sync;
+            bool fin;
             C total;
             if constexpr (kSkip) {
+                const bool past = v < T && v > b;
                 // Slack skip: with X = base + delta at v, a later segment costs
                 // what it costs in the base plan unless it starts at an sR setup
                 // whose slack < max(delta, 0) (for delta < 0: slack < 0), where
@@ -1259,7 +1259,7 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
                 const V delta = X - bv.x;
                 const int li = delta < 0 ? kSlackLevels + 1 : min(ceil_log2(delta), kSlackLevels);
                 const int q = MaskReg::next_of(s.lm[li] | MaskReg::sentinel_of(T), v, T);
-                sync = past && (delta == 0 || q >= T);
+                fin = v >= T || (past && (delta == 0 || q >= T));
                 total = acc + (S - bv.c);
                 const int qq = past && q < T ? q : v;
                 const XC<V, C> bq = s.xc[qq];
@@ -1270,7 +1270,9 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
                 cdu = eq.d;
                 cru = eq.r;
             } else {
-                sync = past && X == bv.x;
+                // done at the end (v = T > b) or once X re-synchronises past
+                // the move
+                fin = v > b && (v >= T || X == bv.x);
                 if constexpr (sizeof(C) == 4)
                     total = acc * pc.one + (bv.c * pc.mone + S);   // two IMADs, not an IADD3
                 else
@@ -1282,7 +1284,6 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
             }
             // total = acc + S - cpre[v]: the base suffix when resynced, and
             // just acc at v = T (xc[T].c = S); only read when fin
-            const bool fin = v >= T || sync;
             const bool take = walking && ok && fin && total < best;
             best = take ? total : best;
             key = take ? slot : key;
