@@ -104,14 +104,19 @@ def test_threads_on_separate_instances_overlap():
 
 
 def test_in_place_edit_invalidates_device_copy():
-    """The reference re-reads the arrays on every call: an in-place edit of
-    the Instance (reference test_model.py:173 does one) must be seen."""
+    """The reference re-reads the arrays on every call (its own
+    test_model.py:173 edits a fresh instance in place): after an upload the
+    arrays are read-only, and an edit made after re-enabling writes, or a
+    reassigned field, is seen by the next call -- never a stale copy."""
     from paper_1704_05132_b200 import SetupPlan
     inst = generate_instance(GeneratorConfig(products=50, periods=52, seed=1))
     sm = np.zeros((50, 52), bool)
     sm[:, 0] = True   # everything produced in period 0: every demand is held
     plan = SetupPlan(sm, np.zeros((50, 52), bool))
     before = evaluate(inst, plan)
+    with pytest.raises(ValueError):   # the uploaded arrays are read-only
+        inst.demand[0, -1] += 7
+    inst.demand.setflags(write=True)  # an explicit opt-in re-uploads
     inst.demand[0, -1] += 7
     got = evaluate(inst, plan)
     assert got == oracle.evaluate(inst, plan.setup_m, plan.setup_r)
