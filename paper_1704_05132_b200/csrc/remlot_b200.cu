@@ -376,14 +376,19 @@ template <> struct VndMinBlocks<int32_t, int32_t, MaskSmem> { static constexpr i
 #ifndef RL_SMEM16_MINB
 #define RL_SMEM16_MINB 5   // 16-bit rows: 9.8 KB shared per warp at T = 520
 #endif
+#ifndef RL_REG_SKIP_MINB
+#define RL_REG_SKIP_MINB 6   // latency-bound launches (slack skip): more registers, measured C2 -4%
+#endif
 #ifdef RL_VND_MINB
-#define RL_VND_MINB_OF(V, C, M, SB) RL_VND_MINB
+#define RL_VND_MINB_OF(V, C, M, SB, SKIP) RL_VND_MINB
 #else
-#define RL_VND_MINB_OF(V, C, M, SB) \
-    (SB == 2 ? RL_SMEM16_MINB : VndMinBlocks<V, C, M>::value)
+#define RL_VND_MINB_OF(V, C, M, SB, SKIP)                                                      \
+    (SB == 2 ? RL_SMEM16_MINB                                                                \
+     : (SKIP && VndMinBlocks<V, C, M>::value == RL_REG_MINB) ? RL_REG_SKIP_MINB            \
+                                                              : VndMinBlocks<V, C, M>::value)
 #endif
 template <typename V, typename C, typename Mask, bool Skip, int SB = (int)sizeof(V)>
-__global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask, SB)) k_vnd(InstView<V> in, const uint8_t *sm_in,
+__global__ void __launch_bounds__(128, RL_VND_MINB_OF(V, C, Mask, SB, Skip)) k_vnd(InstView<V> in, const uint8_t *sm_in,
                                              const uint8_t *sr_in, uint8_t *sm_out,
                                              uint8_t *sr_out, int k_max, VndOut o)
 {
