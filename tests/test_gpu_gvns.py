@@ -223,3 +223,34 @@ def test_gvns_graph_replay_across_runs_on_one_handle():
     gvns(inst, SolverConfig(seed=0, max_rounds=7, **base))
     res = gvns(inst, SolverConfig(seed=0, max_rounds=20, **base))
     assert res.cost == g["cost"] and _plan_sha(res.plan) == g["plan_sha"]
+
+
+def test_gvns_zero_rounds_and_spent_budget_return_the_start():
+    """gvns.py:200-206: the loop checks the budget and the round cap before
+    the first round -- max_rounds=0 or a budget already spent gives the
+    lot-for-lot start with 0 rounds (the device-resident loop is not
+    entered)."""
+    from paper_1704_05132_b200 import evaluate
+    inst = generate_instance(GeneratorConfig(products=50, periods=52, seed=4))
+    init = initial_solution(inst)
+    for cfg in (SolverConfig(t_max=1e9, workers=2, seed=0, max_rounds=0),
+                SolverConfig(t_max=1e-9, workers=2, seed=0)):
+        res = gvns(inst, cfg)
+        assert res.rounds == 0 and res.shake_calls == 0
+        assert res.cost == evaluate(inst, init)
+        assert np.array_equal(res.plan.setup_m, init.setup_m)
+        assert np.array_equal(res.plan.setup_r, init.setup_r)
+
+
+def test_gvns_device_loop_replays_with_new_caps():
+    """The device loop's graph is built once per begin and replayed with the
+    round cap read from device memory: consecutive capped runs on one
+    Instance match the reference's round-capped goldens (gvns_k1000.json)."""
+    with open(os.path.join(GOLDEN, "gvns_k1000.json")) as f:
+        gold = json.load(f)
+    inst = generate_instance(GeneratorConfig(products=1000, periods=52, seed=0))
+    for name, R in (("W2_R150", 150), ("W2_R20", 20), ("W2_R150", 150)):
+        res = gvns(inst, SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=2, seed=0,
+                                      max_rounds=R))
+        assert res.rounds == R and res.cost == gold[name]["cost"]
+        assert _plan_sha(res.plan) == gold[name]["plan_sha"]
