@@ -27,6 +27,7 @@ GOLD = os.path.join(ROOT, "tests", "golden", "paper_scale_cpu.json")
 mode = sys.argv[1]
 n_inst = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 t_max = float(sys.argv[3]) if len(sys.argv) > 3 else 60.0
+first = int(sys.argv[4]) if len(sys.argv) > 4 else 0   # cpu: append instances first..
 
 if mode == "cpu":
     import remlot as pkg
@@ -55,7 +56,11 @@ gold = None
 if mode == "gpu":
     with open(GOLD) as f:
         gold = json.load(f)
-for i in range(n_inst):
+    n_inst = min(n_inst, len(gold["instances"]))
+elif first and os.path.exists(GOLD):
+    with open(GOLD) as f:
+        out = json.load(f)   # append to the earlier cells
+for i in range(first, n_inst):
     name = f"gen{2000 + i}"
     inst = pkg.generate_instance(pkg.GeneratorConfig(products=300, periods=52, seed=2000 + i))
     row = {}
