@@ -47,6 +47,7 @@ struct GvnsArgs {
     int64_t *fbpcost;                 // fb_slots x K
     int *queue;
     int64_t *rbest;                   // B x 3: per batch round best (cost, global worker, slot)
+    void *pfx;                        // K x 2(T+1) V: cd[0..T], cr[0..T] (prefix sums, shake test)
 };
 
 enum {
@@ -265,6 +266,46 @@ __device__ void shake_fallback(const InstView<V> &in, const GvnsArgs &g, int w, 
     __syncwarp();
 }
 
+// Per-product prefix sums cd[t] = sum_{i<t} D, cr[t] = sum_{i<t} R (t <= T)
+// for the shake's feasibility test, computed once per rl_gvns_begin (one
+// warp per product) instead of for every touched product of every redraw.
+template <typename V>
+__global__ void k_gvns_prefix(InstView<V> in, V *pfx)
+{
+    const int lane = threadIdx.x & 31, T = in.T;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < in.K;
+         k += nw) {
+        V *cd = pfx + k * 2 * (T + 1), *cr = cd + T + 1;
+        V cdc = 0, crc = 0;
+        if (lane == 0) {
+            cd[0] = 0;
+            cr[0] = 0;
+        }
+        for (int base = 0; base < T; base += 32) {
+            const int t = base + lane;
+            V d = t < T ? in.dem[k * T + t] : V(0);
+            V r = t < T ? in.ret[k * T + t] : V(0);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const V od = __shfl_up_sync(FULL, d, off), orr = __shfl_up_sync(FULL, r, off);
+                if (lane >= off) {
+                    d += od;
+                    r += orr;
+                }
+            }
+            d += cdc;
+            r += crc;
+            if (t < T) {
+                cd[t + 1] = d;
+                cr[t + 1] = r;
+            }
+            cdc = __shfl_sync(FULL, d, 31);
+            crc = __shfl_sync(FULL, r, 31);
+        }
+    }
+}
+
 // One warp per worker: lane 0 runs the (inherently sequential) numpy-exact
 // draw and the flips; the other lanes pull the touched products' rows
 // (incumbent bits, demand, returns) into L1 with coalesced loads first, so
@@ -304,7 +345,6 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
     int64_t *tp = g.tp + (int64_t)w * g.tcap;
     uint32_t *tw = g.tw + (int64_t)w * g.tcap * 2 * NW;
     uint64_t *table = g.table + (int64_t)w * g.tsize;
-    V *drow = nullptr;
     if (g.shake_bytes) {
         unsigned char *b = shk + (size_t)(threadIdx.x >> 5) * g.shake_bytes;
         table = (uint64_t *)b;
@@ -314,8 +354,6 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
         tp = (int64_t *)b;
         b += align16((size_t)g.tcap * 8);
         tw = (uint32_t *)b;
-        b += align16((size_t)g.tcap * 2 * NW * 4);
-        drow = (V *)b;   // the touched products' demand / returns rows
     }
     for (int attempt = 0; attempt < 50; ++attempt) {   // _SHAKE_REDRAWS (gvns.py:29, :114)
         int n = 0;
@@ -363,50 +401,10 @@ __global__ void k_shake(InstView<V> in, GvnsArgs g, int64_t round_arg, int64_t m
                     const int t = (int)(rem % T);
                     row[(p < g.KT ? 0 : NW) + (t >> 5)] ^= 1u << (t & 31);
                 }
-            if (drow) {   // prefix sums of the rows, then the warp test
-                V *cd = drow + (int64_t)j * 2 * (T + 1), *cr = cd + T + 1;
-                V cdc = 0, crc = 0;
-                if (lane == 0) {
-                    cd[0] = 0;
-                    cr[0] = 0;
-                }
-                for (int base = 0; base < T; base += 32) {
-                    const int t = base + lane;
-                    V d = t < T ? in.dem[k * T + t] : V(0);
-                    V r = t < T ? in.ret[k * T + t] : V(0);
-#pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const V od = __shfl_up_sync(FULL, d, off), orr = __shfl_up_sync(FULL, r, off);
-                        if (lane >= off) {
-                            d += od;
-                            r += orr;
-                        }
-                    }
-                    d += cdc;
-                    r += crc;
-                    if (t < T) {
-                        cd[t + 1] = d;
-                        cr[t + 1] = r;
-                    }
-                    cdc = __shfl_sync(FULL, d, 31);
-                    crc = __shfl_sync(FULL, r, 31);
-                }
-                __syncwarp();
-                ok = warp_row_feasible<V>(cd, cr, T, row, NW, lane);
-            } else {
-                for (int t = lane; t < T; t += 32) {   // warm L1 for lane 0's walk
-                    (void)__ldg(in.dem + k * T + t);
-                    (void)__ldg(in.ret + k * T + t);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    const V *dd = in.dem + k * T, *rr = in.ret + k * T;
-                    ok = row_feasible<V>(dd, rr, T,
-                                         [&](int q) { return (row[q >> 5] >> (q & 31)) & 1u; },
-                                         [&](int q) { return (row[NW + (q >> 5)] >> (q & 31)) & 1u; });
-                }
-                ok = __shfl_sync(FULL, (int)ok, 0);
-            }
+            // the warp test over the product's prefix sums (k_gvns_prefix)
+            const V *cd = (const V *)g.pfx + k * 2 * (T + 1);
+            __syncwarp();
+            ok = warp_row_feasible<V>(cd, cd + T + 1, T, row, NW, lane);
         }
         ok = __shfl_sync(FULL, (int)ok, 0);
         if (ok) {
@@ -820,6 +818,16 @@ static int gv_launch_shake(rl_instance *h, GvnsState *gs, int64_t round_arg,
     return 0;
 }
 
+template <typename V, typename C>
+static int gv_launch_prefix(rl_instance *h, GvnsState *gs)
+{
+    const int64_t warps = h->K < 148 * 64 ? h->K : 148 * 64;
+    k_gvns_prefix<V><<<(unsigned)((warps + 7) / 8), 256, 0, h->stream>>>(view<V>(h),
+                                                                         (V *)gs->a.pfx);
+    CKL();
+    return 0;
+}
+
 extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64_t worker_offset,
                                    int k_max, int k_vnd_max, uint64_t seed, const uint8_t *sm,
                                    const uint8_t *sr, int64_t *inc_cost)
@@ -859,8 +867,7 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
         a.tsize = (int)(choice_table_mask(keff_max) + 1);
         {
             const size_t b = align16((size_t)a.tsize * 8) + align16((size_t)a.kcap * 8) +
-                             align16((size_t)a.tcap * 8) + align16((size_t)a.tcap * 2 * NW * 4) +
-                             align16((size_t)a.tcap * 2 * (T + 1) * h->vbytes);
+                             align16((size_t)a.tcap * 8) + align16((size_t)a.tcap * 2 * NW * 4);
             a.shake_bytes = 4 * b <= 48 * 1024 ? (int)b : 0;
         }
         // fallback plans: enough slots for one round's workers (speculative
@@ -904,6 +911,8 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
         if (e == cudaSuccess) e = gv_alloc(gs, &a.fbpcost, (size_t)a.fb_slots * K * 8);
         if (e == cudaSuccess) e = gv_alloc(gs, &a.queue, 16);
         if (e == cudaSuccess) e = gv_alloc(gs, &a.rbest, (size_t)batch * 3 * 8);
+        if (e == cudaSuccess)
+            e = gv_alloc(gs, (unsigned char **)&a.pfx, (size_t)K * 2 * (T + 1) * h->vbytes);
         if (e != cudaSuccess) {
             gvns_free(gs);
             h->gv = nullptr;
@@ -928,6 +937,8 @@ extern "C" int rl_gvns_begin_batch(rl_instance *h, int workers, int batch, int64
     CK(cudaMemcpyAsync(a.inc + KT, sr, KT, cudaMemcpyHostToDevice, h->stream));
     int rc = rl_initial_solution_device(h, a.init, a.init + KT, h->stream);
     if (rc)
+        return rc;
+    if ((rc = RL_DISPATCH(h, gv_launch_prefix, h, gs)))
         return rc;
     rc = rl_vnd_device(h, k_vnd_max, a.inc, a.inc + KT, a.F, a.F + KT, h->stream);
     if (rc)
