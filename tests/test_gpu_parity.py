@@ -295,6 +295,45 @@ def test_mixed_width_t520_paths(variant):
     np.testing.assert_array_equal(sm, om)
 
 
+@pytest.mark.parametrize("variant", [2, 130])
+def test_t130_wide_costs_16bit_rows(variant):
+    """The 16-bit-row kernel (T > 63, warp per product: variant bit 2) with
+    costs beyond 32 bits: every third product here has setup costs x 10^3
+    (costs ~2 x 10^10, cpre values far past 2^32); every result equals the
+    oracle's, as on the 8-byte-row layout (variant 130)."""
+    rng = np.random.default_rng(130)
+    K, T = 36, 130
+    inst = generate_instance(GeneratorConfig(products=K, periods=T, seed=13))
+    km, kr = inst.setup_cost_m.copy(), inst.setup_cost_r.copy()
+    km[::3] *= 10**3
+    kr[::3] *= 10**3
+    inst = Instance(K, T, inst.demand, inst.returns, km, kr, inst.holding_cost_m,
+                    inst.holding_cost_r, inst.unit_cost_m, inst.unit_cost_r)
+    assert inst.demand.sum(1).max() < 2**16 and inst.returns.sum(1).max() < 2**16
+    dev = DeviceInstance(inst)
+    dev.set_variant(variant)
+    assert dev.info["value_bytes"] == 4 and dev.info["cost_bytes"] == 8
+    start = initial_solution(inst)
+    s0 = oracle.product_costs(inst, start.setup_m, start.setup_r)
+    assert (s0[::3] >= 2**32).all()
+    plans = [start, type(start)(rng.random((K, T)) < 0.5, rng.random((K, T)) < 0.3)]
+    for plan in plans:
+        for k_max in (2, 4):
+            sm, sr, trace, st = dev.vnd(plan.setup_m, plan.setup_r, k_max)
+            om, orr, ocost, otrace, ost = oracle.vnd(inst, plan.setup_m, plan.setup_r, k_max,
+                                                     threads=8)
+            assert st["cost"] == ocost
+            np.testing.assert_array_equal(trace, otrace)
+            np.testing.assert_array_equal(sm, om)
+            np.testing.assert_array_equal(sr, orr)
+            assert st["evals_reference"] == ost["evals"]
+    sm, sr, trace, st = dev.vnd_host(inst, start.setup_m, start.setup_r)
+    om, orr, ocost, otrace, _ = oracle.vnd(inst, start.setup_m, start.setup_r, threads=8)
+    assert st["cost"] == ocost
+    np.testing.assert_array_equal(trace, otrace)
+    np.testing.assert_array_equal(sm, om)
+
+
 @pytest.mark.parametrize("over", [False, True])
 @pytest.mark.parametrize("T", [52, 300])
 def test_int32_coefficient_bound(T, over):
