@@ -214,6 +214,17 @@ struct Slot {
 #ifndef RL_WORD_ENUM_MIN_T
 #define RL_WORD_ENUM_MIN_T 128
 #endif
+// Walk steps per queue iteration (between the ballot / refill control):
+// register rows 2 (measured C3 17.6 -> 16.7 ms, T=63 12.2 -> 11.6, C2 0.59 ->
+// 0.57, GVNS +3-5%; 3: C2 and GVNS slower, 4: +3-9%), shared-memory rows 1
+// (2 and 3 within noise at C4, 4: +11%).  A lane whose walk ends in the
+// first step issues the second one discarded, like an idle lane.
+#ifndef RL_WALK_STEPS_REG
+#define RL_WALK_STEPS_REG 2
+#endif
+#ifndef RL_WALK_STEPS_SMEM
+#define RL_WALK_STEPS_SMEM 1
+#endif
 #ifndef RL_REFILL_MIN
 #define RL_REFILL_MIN 16   // measured: 1 -> 20.1, 8 -> 19.1, 16 -> 18.8, 24 -> 18.9 ms at C3
 #endif
@@ -1216,78 +1227,81 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
         // Issued unconditionally (no divergent branch and reconvergence per
         // iteration): idle lanes step from period T - 1 (a valid query whose
         // next setup is the end, T) and their results are discarded.
-        const bool walking = state == 2;
-        if (RL_STEP_BRANCH == 0 || walking) {
+#pragma unroll
+        for (int rep = 0; rep < (kRegMask ? RL_WALK_STEPS_REG : RL_WALK_STEPS_SMEM); ++rep) {
+            const bool walking = state == 2;
+            if (RL_STEP_BRANCH == 0 || walking) {
 #ifdef RL_WALK_STATS
-            ws_cur += walking;
-            ws_lane += walking;
+                ws_cur += walking;
+                ws_lane += walking;
 #endif
-            if (!walking)
-                u = T - 1;   // a valid start for the discarded step
-            // register masks test the candidate's bits directly (measured
-            // faster); shared-memory masks carry the kind from the nx table
-            int tv = 0, v;
-            bool mu, ru;
-            if constexpr (kRegMask) {
-                v = pw.next(u + 1);
-                mu = pw.m(u);
-                ru = pw.r(u);
-            } else {
-                v = pw.next_t(u + 1, tv);
-                mu = tu & 1;
-                ru = tu >> 1;
-            }
-            const DR<V> ev = s.dr[v];
-            C c;
-            V xr;
-            const bool ok = seg_cost<V, C>(cdu, cru, ev.d, u, mu, ru, X, pc, c, xr);
-            const XC<V, C> bv = s.xc[v];   // v <= T; xc[T].c = S
-            acc += c;
-            X += xr;
-            // past the move the rows equal the base plan's; only X may differ
-            bool fin;
-            C total;
-            if constexpr (kSkip) {
-                const bool past = v < T && v > b;
-                // Slack skip: with X = base + delta at v, a later segment costs
-                // what it costs in the base plan unless it starts at an sR setup
-                // whose slack < max(delta, 0) (for delta < 0: slack < 0), where
-                // min(seg, avail) changes.  Jump to the next setup of the
-                // slack-level mask bounding that set (false positives are just
-                // walked exactly), adding the base cost of the segments skipped;
-                // no such setup left = the rest of the base plan (resync).
-                const V delta = X - bv.x;
-                const int li = delta < 0 ? kSlackLevels + 1 : min(ceil_log2(delta), kSlackLevels);
-                const int q = MaskReg::next_of(s.lm[li] | MaskReg::sentinel_of(T), v, T);
-                fin = v >= T || (past && (delta == 0 || q >= T));
-                total = acc + (S - bv.c);
-                const int qq = past && q < T ? q : v;
-                const XC<V, C> bq = s.xc[qq];
-                const DR<V> eq = s.dr[qq];
-                acc += bq.c - bv.c;   // 0 unless past (qq == v otherwise)
-                X = past ? bq.x + delta : X;
-                u = qq;
-                cdu = eq.d;
-                cru = eq.r;
-            } else {
-                // done at the end (v = T > b) or once X re-synchronises past
-                // the move
-                fin = v > b && (v >= T || X == bv.x);
-                if constexpr (sizeof(C) == 4)
-                    total = acc * pc.one + (bv.c * pc.mone + S);   // two IMADs, not an IADD3
-                else
+                if (!walking)
+                    u = T - 1;   // a valid start for the discarded step
+                // register masks test the candidate's bits directly (measured
+                // faster); shared-memory masks carry the kind from the nx table
+                int tv = 0, v;
+                bool mu, ru;
+                if constexpr (kRegMask) {
+                    v = pw.next(u + 1);
+                    mu = pw.m(u);
+                    ru = pw.r(u);
+                } else {
+                    v = pw.next_t(u + 1, tv);
+                    mu = tu & 1;
+                    ru = tu >> 1;
+                }
+                const DR<V> ev = s.dr[v];
+                C c;
+                V xr;
+                const bool ok = seg_cost<V, C>(cdu, cru, ev.d, u, mu, ru, X, pc, c, xr);
+                const XC<V, C> bv = s.xc[v];   // v <= T; xc[T].c = S
+                acc += c;
+                X += xr;
+                // past the move the rows equal the base plan's; only X may differ
+                bool fin;
+                C total;
+                if constexpr (kSkip) {
+                    const bool past = v < T && v > b;
+                    // Slack skip: with X = base + delta at v, a later segment costs
+                    // what it costs in the base plan unless it starts at an sR setup
+                    // whose slack < max(delta, 0) (for delta < 0: slack < 0), where
+                    // min(seg, avail) changes.  Jump to the next setup of the
+                    // slack-level mask bounding that set (false positives are just
+                    // walked exactly), adding the base cost of the segments skipped;
+                    // no such setup left = the rest of the base plan (resync).
+                    const V delta = X - bv.x;
+                    const int li = delta < 0 ? kSlackLevels + 1 : min(ceil_log2(delta), kSlackLevels);
+                    const int q = MaskReg::next_of(s.lm[li] | MaskReg::sentinel_of(T), v, T);
+                    fin = v >= T || (past && (delta == 0 || q >= T));
                     total = acc + (S - bv.c);
-                u = v;
-                tu = tv;
-                cdu = ev.d;
-                cru = ev.r;
+                    const int qq = past && q < T ? q : v;
+                    const XC<V, C> bq = s.xc[qq];
+                    const DR<V> eq = s.dr[qq];
+                    acc += bq.c - bv.c;   // 0 unless past (qq == v otherwise)
+                    X = past ? bq.x + delta : X;
+                    u = qq;
+                    cdu = eq.d;
+                    cru = eq.r;
+                } else {
+                    // done at the end (v = T > b) or once X re-synchronises past
+                    // the move
+                    fin = v > b && (v >= T || X == bv.x);
+                    if constexpr (sizeof(C) == 4)
+                        total = acc * pc.one + (bv.c * pc.mone + S);   // two IMADs, not an IADD3
+                    else
+                        total = acc + (S - bv.c);
+                    u = v;
+                    tu = tv;
+                    cdu = ev.d;
+                    cru = ev.r;
+                }
+                // total = acc + S - cpre[v]: the base suffix when resynced, and
+                // just acc at v = T (xc[T].c = S); only read when fin
+                const bool take = walking && ok && fin && total < best;
+                best = take ? total : best;
+                key = take ? slot : key;
+                state = walking && ok && !fin ? 2 : 0;
             }
-            // total = acc + S - cpre[v]: the base suffix when resynced, and
-            // just acc at v = T (xc[T].c = S); only read when fin
-            const bool take = walking && ok && fin && total < best;
-            best = take ? total : best;
-            key = take ? slot : key;
-            state = walking && ok && !fin ? 2 : 0;
         }
         const unsigned m = __ballot_sync(FULL, state == 0);
         const bool more = m != FULL || next * nw + wi < n;
