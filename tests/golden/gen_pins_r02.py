@@ -26,6 +26,9 @@ Outputs (small JSON under tests/golden/):
   int64_k10000.json  K=10,000 T=52 instances whose cost bound forces the
                      int64-cost path (int32 and int64 values)
   gvns_c5.json       K=1,000 T=52 gvns(seed 0): W=128 x 4 and W=1,024 x 2 rounds
+  gvns_long.json     round-capped live gvns at horizons past the register
+                     rows (T = 100, 300, 520: shared-memory rows in the
+                     device shake / VND tasks) and with int64 costs
 """
 
 import hashlib
@@ -132,7 +135,36 @@ def gen_c5():
         dump("gvns_c5.json", out)
 
 
+def gen_long():
+    from remlot import _kernels
+    _kernels.warm_up()
+    cases = {
+        "K40_T100_W2_R30": (GeneratorConfig(products=40, periods=100, seed=11), 2, 30),
+        "K16_T300_W3_R12": (GeneratorConfig(products=16, periods=300, seed=12), 3, 12),
+        "K12_T520_W2_R8": (GeneratorConfig(products=12, periods=520, seed=13), 2, 8),
+        "K20_T100_c64_W2_R10": (GeneratorConfig(products=20, periods=100, seed=14,
+                                                setup_cost_range=(50_000_000, 200_000_000)),
+                                2, 10),
+    }
+    out = {}
+    for name, (gc, W, R) in cases.items():
+        inst = generate_instance(gc)
+        cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=W, seed=5,
+                           max_rounds=R, vnd_mode="serial", parallelism=1)
+        t0 = time.time()
+        res = gvns(inst, cfg)
+        out[name] = dict(products=gc.products, periods=gc.periods, seed=gc.seed,
+                         setup_cost_range=list(gc.setup_cost_range), workers=W, rounds=R,
+                         cost=int(res.cost), rounds_done=res.rounds,
+                         shake_calls=res.shake_calls,
+                         plan_sha=plan_sha(res.plan.setup_m, res.plan.setup_r),
+                         instance_sha=sha(inst.demand, inst.returns),
+                         wall_s=round(time.time() - t0, 1))
+        print("long", name, res.cost, res.rounds, res.shake_calls, time.time() - t0, flush=True)
+    dump("gvns_long.json", out)
+
+
 if __name__ == "__main__":
-    jobs = dict(c4=gen_c4, n2=gen_n2, int64=gen_int64, c5=gen_c5)
+    jobs = dict(c4=gen_c4, n2=gen_n2, int64=gen_int64, c5=gen_c5, long=gen_long)
     for a in sys.argv[1:]:
         jobs[a]()

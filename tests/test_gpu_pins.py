@@ -149,3 +149,21 @@ def test_c5_replicas_match_reference(name, W, R):
                                   max_rounds=R))
     assert res.cost == g["cost"] and res.rounds == R and res.shake_calls == g["shake_calls"]
     assert _plan_sha(res.plan.setup_m, res.plan.setup_r) == g["plan_sha"]
+
+
+@pytest.mark.parametrize("name", ["K40_T100_W2_R30", "K16_T300_W3_R12", "K12_T520_W2_R8",
+                                  "K20_T100_c64_W2_R10"])
+def test_gvns_long_horizons_match_reference(name):
+    """Round-capped live-reference gvns past the register rows (T = 100,
+    300, 520: the device shake's multi-word rows and the shared-memory-row
+    VND tasks) and with int64 costs (setup costs 5e7-2e8)."""
+    g = _load("gvns_long.json")[name]
+    inst = generate_instance(GeneratorConfig(products=g["products"], periods=g["periods"],
+                                             seed=g["seed"],
+                                             setup_cost_range=tuple(g["setup_cost_range"])))
+    assert _sha(inst.demand, inst.returns) == g["instance_sha"]
+    res = gvns(inst, SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=g["workers"], seed=5,
+                                  max_rounds=g["rounds"]))
+    assert res.cost == g["cost"]
+    assert res.rounds == g["rounds_done"] and res.shake_calls == g["shake_calls"]
+    assert _plan_sha(res.plan.setup_m, res.plan.setup_r) == g["plan_sha"]
