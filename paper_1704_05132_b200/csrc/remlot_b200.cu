@@ -773,8 +773,8 @@ __global__ void k_list_moves(int nbh, int T, const uint8_t *sm, const uint8_t *s
 // ------------------------------------------------------------------ handle
 
 #ifndef RL_E2E_CHUNKS
-#define RL_E2E_CHUNKS 4
-#endif
+#define RL_E2E_CHUNKS 3   // measured at C3 (geometric, ratio 2): 2 / 3 / 4 / 6 / 8 chunks
+#endif                    // 17.93 / 17.62 / 17.90 / 18.14 / 18.57 ms per e2e step
 constexpr int kMaxChunks = RL_E2E_CHUNKS;   // rl_vnd_host pipeline depth (<= 12: h->ints)
 
 struct rl_instance {
@@ -1622,12 +1622,20 @@ __global__ void k_check_narrow(int64_t lo, int64_t hi, int T, int64_t K, const i
 #ifndef RL_E2E_GEOM
 #define RL_E2E_GEOM 1   // measured: C3 e2e 20.05 -> 19.90 ms
 #endif
+#ifndef RL_E2E_RATIO
+#define RL_E2E_RATIO 2   // chunk-size ratio; 3 / 4 measured 17.87 / 17.79 ms with 3 chunks
+#endif
 static inline int64_t chunk_lo(int64_t K, int c, int n)
 {
     if (!RL_E2E_GEOM || n <= 1)
         return K * c / n;
-    const int64_t total = ((int64_t)1 << n) - 1;   // 1 + 2 + ... + 2^(n-1)
-    return K * (((int64_t)1 << c) - 1) / total;
+    int64_t pc = 1, pn = 1;   // r^c, r^n: chunk c spans [r^c - 1, r^(c+1) - 1) / (r^n - 1)
+    for (int i = 0; i < n; ++i) {
+        if (i < c)
+            pc *= RL_E2E_RATIO;
+        pn *= RL_E2E_RATIO;
+    }
+    return K * (pc - 1) / (pn - 1);
 }
 
 template <typename V, typename C, typename Mask>
