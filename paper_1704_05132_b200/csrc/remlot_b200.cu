@@ -1699,14 +1699,17 @@ extern "C" int rl_vnd_host(rl_instance *h, int k_max, const int64_t *demand,
     CK(cudaStreamWaitEvent(sc, start, 0));
     CK(cudaStreamWaitEvent(s1, start, 0));
     const int64_t *cost[6] = {setup_m, setup_r, hold_m, hold_r, unit_m, unit_r};
-    for (int i = 0; i < 6; ++i)
-        CK(cudaMemcpyAsync(h->cost6 + i * K, cost[i], K * 8, cudaMemcpyHostToDevice, sc));
     CK(cudaMemsetAsync(h->ints, 0, 16 * sizeof(int), sc));
     CK(cudaMemsetAsync(h->bounds, 0, 2 * sizeof(unsigned long long), sc));
     CK(cudaMemsetAsync(h->trace_dec, 0, (size_t)h->cap_sweeps * k_max * 8, sc));
     for (int c = 0; c < nchunks; ++c) {
         const int64_t lo = chunk_lo(K, c, nchunks), hi = chunk_lo(K, c + 1, nchunks);
         const size_t off = (size_t)lo * T, n = (size_t)(hi - lo) * T;
+        // the chunk's slice of the six cost vectors (the first chunk's
+        // kernel needs only its own products' costs)
+        for (int i = 0; i < 6; ++i)
+            CK(cudaMemcpyAsync(h->cost6 + i * K + lo, cost[i] + lo, (size_t)(hi - lo) * 8,
+                               cudaMemcpyHostToDevice, sc));
         CK(cudaMemcpyAsync(h->dem64 + off, demand + off, n * 8, cudaMemcpyHostToDevice, sc));
         CK(cudaMemcpyAsync(h->ret64 + off, returns + off, n * 8, cudaMemcpyHostToDevice, sc));
         CK(cudaMemcpyAsync(h->plan + off, sm_in + off, n, cudaMemcpyHostToDevice, sc));
