@@ -304,6 +304,9 @@ __device__ inline bool vnd_product(const Slot<V, C, SB> &s, Mask &mk, int T, con
         for (int nbh = 1; nbh <= k_max; ++nbh) {
             if (dirty) {
                 base_pass<V, C, Mask, Skip>(s, mk, T, pc, lane, S);
+#ifdef RL_BASE_TWICE   // measurement only: the base pass's share of the descent
+                base_pass<V, C, Mask, Skip>(s, mk, T, pc, lane, S);
+#endif
                 dirty = false;
             }
             C best;

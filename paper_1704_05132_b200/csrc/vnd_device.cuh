@@ -700,6 +700,125 @@ __device__ inline void stage_plain(const Slot<V, C, SB> &s, const V *dem, const 
 
 // --------------------------------------------------------- base pass
 
+// Slack-level masks for the delta-walk skip (scan_pass) from the slk row
+// base_pass wrote: lane l owns periods l and l + 32, so each ballot yields
+// one 32-bit half.
+template <typename V, typename C, int SB, typename Mask>
+__device__ inline void build_slack_masks(const Slot<V, C, SB> &s, const Mask &mk, int T, int lane)
+{
+    const V INF = VInf<V>::value;
+    __syncwarp();
+    const V s0 = lane < T ? s.slk[lane] : INF;
+    const V s1 = lane + 32 < T ? s.slk[lane + 32] : INF;
+    uint64_t mine = 0;
+#pragma unroll
+    for (int j = 0; j <= kSlackLevels + 1; ++j) {
+        if (j == kSlackLevels) {
+            if (lane == j)
+                mine = mk.R_mask();   // any delta >= 2^16: every sR setup
+            continue;
+        }
+        const V lim = j < kSlackLevels ? (V(1) << j) : V(0);
+        const uint64_t mk2 = (uint64_t)__ballot_sync(FULL, s0 < lim) |
+                             ((uint64_t)__ballot_sync(FULL, s1 < lim) << 32);
+        if (lane == j)
+            mine = mk2;
+    }
+    if (lane <= kSlackLevels + 1)
+        s.lm[lane] = mine;
+}
+
+// base_pass for register rows (T <= 63: lane l owns periods lL and lL + 1,
+// L = 1 or 2).  The same two steps and scans as the general form, with
+// each owned period's setup kind, next setup and rows read once into
+// registers (step 2 reuses step 1's), next-setup queries by one clz on the
+// bit-reversed rows, and each xc entry written once after the cost scan
+// (no read-modify-write fix-up).
+template <typename V, typename C, bool Skip, int SB>
+__device__ inline bool base_pass_reg(const Slot<V, C, SB> &s, const MaskReg &mk, int T,
+                                     const ProductCosts<C> &pc, int lane, C &S)
+{
+    const int L = (T + 31) >> 5;
+    const uint64_t SRv = __brevll(mk.M | mk.R | mk.sentinel());
+    const V INF = VInf<V>::value;
+    bool su[2], mu[2], ru[2];
+    int vv[2];
+    V ed[2], er[2], cdv[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int u = lane * L + j;
+        const bool valid = j < L && u < T;
+        mu[j] = valid && mk.m(u);
+        ru[j] = valid && mk.r(u);
+        su[j] = mu[j] | ru[j];
+        vv[j] = 0;
+        ed[j] = er[j] = cdv[j] = 0;
+        if (su[j]) {
+            vv[j] = u + 1 + __clzll((long long)(SRv << (u + 1)));   // first setup > u (<= T)
+            const DR<V> e = s.dr[u];
+            ed[j] = e.d;
+            er[j] = e.r;
+            cdv[j] = s.dr[vv[j]].d;
+        }
+        if (Skip && valid)
+            s.slk[u] = INF;
+    }
+    V A = 0, B = INF;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+        if (ru[j]) {   // only remanufacturing setups move X
+            const V seg = cdv[j] - ed[j];
+            A += seg;
+            B = vmin<V>(B + seg, er[j]);
+        }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        V a2 = __shfl_up_sync(FULL, A, off), b2 = __shfl_up_sync(FULL, B, off);
+        if (lane >= off) {
+            B = vmin<V>(b2 + A, B);
+            A = a2 + A;
+        }
+    }
+    V pa = __shfl_up_sync(FULL, A, 1), pb = __shfl_up_sync(FULL, B, 1);
+    V X = lane == 0 ? V(0) : vmin<V>(pa, pb);
+    C local = 0;
+    bool ok = true;
+    V xin[2];
+    C cin[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        xin[j] = X;
+        cin[j] = local;
+        if (su[j]) {
+            if (Skip && ru[j])
+                s.slk[lane * L + j] = er[j] - X - (cdv[j] - ed[j]);
+            C c;
+            V xr;
+            ok &= seg_cost<V, C>(ed[j], er[j], cdv[j], lane * L + j, mu[j], ru[j], X, pc, c, xr);
+            local += c;
+            X += xr;
+        }
+    }
+    C incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        C o = __shfl_up_sync(FULL, incl, off);
+        if (lane >= off)
+            incl += o;
+    }
+    const C excl = incl - local;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+        if (su[j])
+            s.xc.set(lane * L + j, xin[j], cin[j] + excl);
+    S = __shfl_sync(FULL, incl, 31);
+    if (lane == 0)
+        s.xc.set(T, V(0), S);   // end entry: a walk reaching T adds S - S
+    const int f = __clzll((long long)SRv);   // first setup (T if none)
+    ok = ok && s.dr[f].d == 0;   // demand before the first setup (_kernels.py:58-60)
+    return __all_sync(FULL, ok);
+}
+
 // Evaluate the current plan: fills xin/cpre at every setup period, returns
 // feasibility and S = sum of segment costs (warp-uniform).  Lane l owns the
 // periods [l*L, l*L+L).  Step 1 composes the (min,+) maps of its setups,
@@ -710,6 +829,15 @@ __device__ inline bool base_pass(const Slot<V, C, SB> &s, const Mask &mk, int T,
 {
     if constexpr (std::is_same<Mask, MaskSmem>::value)
         mk.build_tables(lane);
+#ifndef RL_BASE_REG_GENERIC
+    if constexpr (std::is_same<Mask, MaskReg>::value) {
+        const bool feas = base_pass_reg<V, C, Skip, SB>(s, mk, T, pc, lane, S);
+        if (Skip)
+            build_slack_masks(s, mk, T, lane);
+        __syncwarp();
+        return feas;
+    }
+#endif
     const int L = (T + 31) >> 5;
     const int lo = lane * L, hi = min(lo + L, T);
     const V INF = VInf<V>::value;
@@ -816,29 +944,8 @@ __device__ inline bool base_pass(const Slot<V, C, SB> &s, const Mask &mk, int T,
     const int f = mk.next(0);
     ok = ok && s.dr[f].d == 0;   // demand before the first setup (_kernels.py:58-60)
     const bool feas = __all_sync(FULL, ok);
-    if (kSkip) {
-        // slack-level masks for the delta-walk skip (scan_pass): lane l owns
-        // periods l and l + 32, so each ballot yields one 32-bit half
-        __syncwarp();
-        const V s0 = lane < T ? s.slk[lane] : INF;
-        const V s1 = lane + 32 < T ? s.slk[lane + 32] : INF;
-        uint64_t mine = 0;
-#pragma unroll
-        for (int j = 0; j <= kSlackLevels + 1; ++j) {
-            if (j == kSlackLevels) {
-                if (lane == j)
-                    mine = mk.R_mask();   // any delta >= 2^16: every sR setup
-                continue;
-            }
-            const V lim = j < kSlackLevels ? (V(1) << j) : V(0);
-            const uint64_t mk2 = (uint64_t)__ballot_sync(FULL, s0 < lim) |
-                                 ((uint64_t)__ballot_sync(FULL, s1 < lim) << 32);
-            if (lane == j)
-                mine = mk2;
-        }
-        if (lane <= kSlackLevels + 1)
-            s.lm[lane] = mine;
-    }
+    if (kSkip)
+        build_slack_masks(s, mk, T, lane);
     __syncwarp();
     return feas;
 }
@@ -1347,7 +1454,10 @@ __device__ inline PassResult scan_pass(const Slot<V, C, SB> &s, const Mask &mk, 
                                        const ProductCosts<C> &pc, C S, int nbh, int lane,
                                        C &best_out)
 {
-    const int n = enumerate_moves(s, mk, nbh, T, lane);
+    int n = enumerate_moves(s, mk, nbh, T, lane);
+#ifdef RL_ENUM_TWICE   // measurement only: the enumeration's share of the descent
+    n = enumerate_moves(s, mk, nbh, T, lane);
+#endif
     C best = S;
     int key = 0x7fffffff;
     walk_moves<V, C, Mask, Skip>(s, mk, T, pc, S, nbh, n, lane, 0, 1, best, key);
