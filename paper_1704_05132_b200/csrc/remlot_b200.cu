@@ -299,11 +299,17 @@ __device__ inline bool vnd_product(const Slot<V, C, SB> &s, Mask &mk, int T, con
         return false;
     }
     bool dirty = false;
+    int ma = 0, mb = 0;   // the applied move's periods (a <= b)
     for (;;) {
         bool improved = false;
         for (int nbh = 1; nbh <= k_max; ++nbh) {
             if (dirty) {
-                base_pass<V, C, Mask, Skip>(s, mk, T, pc, lane, S);
+#ifndef RL_NO_REBASE
+                if constexpr (std::is_same<Mask, MaskSmem>::value)
+                    rebase_smem<V, C, SB>(s, mk, T, pc, lane, S, ma, mb);
+                else
+#endif
+                    base_pass<V, C, Mask, Skip>(s, mk, T, pc, lane, S);
 #ifdef RL_BASE_TWICE   // measurement only: the base pass's share of the descent
                 base_pass<V, C, Mask, Skip>(s, mk, T, pc, lane, S);
 #endif
@@ -320,6 +326,9 @@ __device__ inline bool vnd_product(const Slot<V, C, SB> &s, Mask &mk, int T, con
             }
 #endif
             if (r.improved) {
+                const MoveDesc md = slot_move(mk, nbh, r.slot, T);
+                ma = md.p1 >= 0 && md.p1 < md.p0 ? md.p1 : md.p0;
+                mb = md.p1 > md.p0 ? md.p1 : md.p0;
                 apply_slot(mk, nbh, r.slot, T, lane);
                 dirty = true;
                 improved = true;

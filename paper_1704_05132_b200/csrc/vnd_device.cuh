@@ -950,6 +950,90 @@ __device__ inline bool base_pass(const Slot<V, C, SB> &s, const Mask &mk, int T,
     return feas;
 }
 
+// Incremental base pass for shared-memory rows after the applied move
+// rewrote periods a <= b (vnd_product).  The new plan equals the old one
+// before p = prev(a) and, past the first setup v > b where the re-walked X
+// equals the old entering X, everywhere except for a constant shift of the
+// prefix costs -- the resynchronisation the delta walk uses.  So: rebuild
+// nx on [p+1, b], re-walk the move's segments from p writing their
+// {xin, cpre}, add the cost shift to the setups past the resync point (or
+// end the walk at T).  Identical values to a full base_pass (tested: the
+// C4 pins, the long-horizon fuzz and GVNS goldens).  S: the winning total.
+template <typename V, typename C, int SB>
+__device__ inline void rebase_smem(const Slot<V, C, SB> &s, const MaskSmem &mk, int T,
+                                   const ProductCosts<C> &pc, int lane, C &S, int a, int b)
+{
+    const int p = mk.prev(a);
+    {   // next-setup table on [p + 1, b]: a, b (if setups now) or nx[b + 1]
+        const int eb1 = mk.nx[b + 1];
+        const int ka = (int)mk.m(a) | (int)mk.r(a) << 1, kb = (int)mk.m(b) | (int)mk.r(b) << 1;
+        __syncwarp();
+        for (int t = p + 1 + lane; t <= b; t += 32) {
+            int e = eb1;
+            if (kb)
+                e = b | kb << kTypeShift;
+            if (ka && t <= a)
+                e = a | ka << kTypeShift;
+            mk.nx[t] = (uint16_t)e;
+        }
+        __syncwarp();
+    }
+    int u;
+    V X;
+    C acc;
+    if (p >= 0) {   // the prefix before p is unchanged
+        const XC<V, C> e = s.xc[p];
+        u = p;
+        X = e.x;
+        acc = e.c;
+    } else {
+        u = mk.nx[0] & kPeriodMask;
+        X = 0;
+        acc = 0;
+    }
+    const C S_old = s.xc[T].c;
+    bool resync = false;
+    int vs = T;
+    C delta = 0;
+    while (u < T) {
+        const int ty = mk.nx[u] >> kTypeShift;   // u is a setup: its own entry
+        const int v = mk.nx[u + 1] & kPeriodMask;
+        const DR<V> d = s.dr[u];
+        const V cdv = s.dr[v].d;
+        if (lane == 0)
+            s.xc.set(u, X, acc);
+        C c;
+        V xr;
+        seg_cost<V, C>(d.d, d.r, cdv, u, ty & 1, ty >> 1, X, pc, c, xr);
+        acc += c;
+        X += xr;
+        if (v > b && v < T) {
+            const XC<V, C> o = s.xc[v];   // past the move: a setup of both plans
+            if (X == o.x) {
+                resync = true;
+                vs = v;
+                delta = acc - o.c;
+                break;
+            }
+        }
+        u = v;
+    }
+    __syncwarp();
+    C S_new = acc;
+    if (resync) {
+        S_new = S_old + delta;
+        if (delta != C(0))
+            for (int t = vs + lane; t < T; t += 32)
+                if (mk.setup(t))
+                    s.xc.add_c(t, delta);
+    }
+    RL_ASSERT(S_new == S);
+    S = S_new;
+    if (lane == 0)
+        s.xc.set(T, V(0), S);
+    __syncwarp();
+}
+
 // ------------------------------------------------------- move scoring
 
 // A move in reference form (list_moves, _kernels.py:188-258): period p0
