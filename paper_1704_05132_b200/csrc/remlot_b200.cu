@@ -307,6 +307,8 @@ __device__ inline bool vnd_product(const Slot<V, C, SB> &s, Mask &mk, int T, con
 #ifndef RL_NO_REBASE
                 if constexpr (std::is_same<Mask, MaskSmem>::value)
                     rebase_smem<V, C, SB>(s, mk, T, pc, lane, S, ma, mb);
+                else if constexpr (!Skip)
+                    rebase_reg<V, C, SB>(s, mk, T, pc, lane, S, ma, mb);
                 else
 #endif
                     base_pass<V, C, Mask, Skip>(s, mk, T, pc, lane, S);

@@ -1034,6 +1034,76 @@ __device__ inline void rebase_smem(const Slot<V, C, SB> &s, const MaskSmem &mk, 
     __syncwarp();
 }
 
+// The same incremental base pass for register rows (the throughput kernel;
+// the slack-skip kernel rebuilds its slack rows in a full base_pass): the
+// rows are already the new plan's, next setups by clz on the bit-reversed
+// rows, and each lane shifts the prefix costs of its own periods.
+template <typename V, typename C, int SB>
+__device__ inline void rebase_reg(const Slot<V, C, SB> &s, const MaskReg &mk, int T,
+                                  const ProductCosts<C> &pc, int lane, C &S, int a, int b)
+{
+    const uint64_t SRv = __brevll(mk.M | mk.R | mk.sentinel());
+    const int p = mk.prev(a);
+    int u;
+    V X;
+    C acc;
+    if (p >= 0) {   // the prefix before p is unchanged
+        const XC<V, C> e = s.xc[p];
+        u = p;
+        X = e.x;
+        acc = e.c;
+    } else {
+        u = __clzll((long long)SRv);   // first setup (T if none)
+        X = 0;
+        acc = 0;
+    }
+    const C S_old = s.xc[T].c;
+    bool resync = false;
+    int vs = T;
+    C delta = 0;
+    while (u < T) {
+        const int v = u + 1 + __clzll((long long)(SRv << (u + 1)));
+        const DR<V> d = s.dr[u];
+        const V cdv = s.dr[v].d;
+        if (lane == 0)
+            s.xc.set(u, X, acc);
+        C c;
+        V xr;
+        seg_cost<V, C>(d.d, d.r, cdv, u, mk.m(u), mk.r(u), X, pc, c, xr);
+        acc += c;
+        X += xr;
+        if (v > b && v < T) {
+            const XC<V, C> o = s.xc[v];   // past the move: a setup of both plans
+            if (X == o.x) {
+                resync = true;
+                vs = v;
+                delta = acc - o.c;
+                break;
+            }
+        }
+        u = v;
+    }
+    __syncwarp();
+    C S_new = acc;
+    if (resync) {
+        S_new = S_old + delta;
+        if (delta != C(0)) {
+            const int L = (T + 31) >> 5;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int t = lane * L + j;
+                if (j < L && t < T && t >= vs && (mk.m(t) | mk.r(t)))
+                    s.xc.add_c(t, delta);
+            }
+        }
+    }
+    RL_ASSERT(S_new == S);
+    S = S_new;
+    if (lane == 0)
+        s.xc.set(T, V(0), S);
+    __syncwarp();
+}
+
 // ------------------------------------------------------- move scoring
 
 // A move in reference form (list_moves, _kernels.py:188-258): period p0
