@@ -506,12 +506,18 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
         int sweeps = 0, moves = 0, ntot = 0;
         if (feas) {
             bool dirty = false;
+            int ma = 0, mb = 0;   // the applied move's periods (warp 0)
             for (;;) {
                 bool improved = false;
                 for (int nbh = 1; nbh <= k_max; ++nbh) {
                     if (warp == 0) {
-                        if (dirty)
+                        if (dirty) {
+#ifndef RL_NO_REBASE
+                            rebase_smem<V, C, (int)sizeof(V)>(s, mk, T, pc, lane, S, ma, mb);
+#else
                             base_pass<V, C, MaskSmem, false>(s, mk, T, pc, lane, S);
+#endif
+                        }
                         const int n = enumerate_moves(s, mk, nbh, T, lane);
                         if (lane == 0) {
                             sh_n = n;
@@ -537,6 +543,9 @@ __global__ void __launch_bounds__(128) k_vnd_cta(InstView<V> in, const uint8_t *
                         warp_argmin(b, kk);
                         if (kk != 0x7fffffff) {
                             MaskSmem mw = mk;
+                            const MoveDesc md = slot_move(mw, nbh, kk, T);
+                            ma = md.p1 >= 0 && md.p1 < md.p0 ? md.p1 : md.p0;
+                            mb = md.p1 > md.p0 ? md.p1 : md.p0;
                             apply_slot(mw, nbh, kk, T, lane);
                             if (lane == 0) {
                                 if (sweeps < o.cap_sweeps)

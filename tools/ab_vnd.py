@@ -12,7 +12,7 @@ from paper_1704_05132_b200._native import DeviceInstance  # noqa: E402
 
 SIZES = {"c3": (100000, 52), "c2": (1000, 52), "c4": (10000, 520), "t63": (50000, 63),
          "t30": (100000, 30), "k20k": (20000, 52), "k50k": (50000, 52), "k200k": (200000, 52),
-         "k12k": (12500, 52), "k25k": (25000, 52), "t200": (20000, 200)}
+         "k12k": (12500, 52), "k25k": (25000, 52), "t200": (20000, 200), "k100t520": (100, 520), "k296t520": (296, 520)}
 wl = sys.argv[1]
 K, T = SIZES[wl]
 dev = DeviceInstance.generate(GeneratorConfig(products=K, periods=T, seed=0))
