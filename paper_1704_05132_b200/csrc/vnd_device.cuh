@@ -216,14 +216,16 @@ struct Slot {
 #endif
 // Walk steps per queue iteration (between the ballot / refill control):
 // register rows 2 (measured C3 17.6 -> 16.7 ms, T=63 12.2 -> 11.6, C2 0.59 ->
-// 0.57, GVNS +3-5%; 3: C2 and GVNS slower, 4: +3-9%), shared-memory rows 1
-// (2 and 3 within noise at C4, 4: +11%).  A lane whose walk ends in the
-// first step issues the second one discarded, like an idle lane.
+// 0.57, GVNS +3-5%; 3: C2 and GVNS slower, 4: +3-9%), shared-memory rows 2
+// (after the incremental re-base: C4 114.5 -> 112.6-114.5 ms, T=200 -2%,
+// K=100 T=520 (CTA per product) 12.0 -> 10.5 ms; within noise at C4 with
+// the full base pass; 4: +11%).  A lane whose walk ends in the first step
+// issues the second one discarded, like an idle lane.
 #ifndef RL_WALK_STEPS_REG
 #define RL_WALK_STEPS_REG 2
 #endif
 #ifndef RL_WALK_STEPS_SMEM
-#define RL_WALK_STEPS_SMEM 1
+#define RL_WALK_STEPS_SMEM 2
 #endif
 #ifndef RL_REFILL_MIN
 #define RL_REFILL_MIN 16   // measured: 1 -> 20.1, 8 -> 19.1, 16 -> 18.8, 24 -> 18.9 ms at C3
