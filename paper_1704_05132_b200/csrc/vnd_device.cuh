@@ -229,6 +229,9 @@ struct Slot {
 #ifndef RL_WALK_STEPS_SMEM
 #define RL_WALK_STEPS_SMEM 2
 #endif
+#ifndef RL_REFILL_MIN_SMEM   // shared-memory rows, two walk steps per iteration: measured
+#define RL_REFILL_MIN_SMEM 12   // C4 8 / 12 / 16 / 24: 109.8-111.3 / 109.5-110.4 / 110.6-111.9 / 120 ms
+#endif
 #ifndef RL_REFILL_MIN
 #define RL_REFILL_MIN 16   // measured: 1 -> 20.1, 8 -> 19.1, 16 -> 18.8, 24 -> 18.9 ms at C3
 #endif
@@ -1572,7 +1575,7 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
         const bool more = m != FULL || next * nw + wi < n;
         // refill idle lanes in batches (the set-up branch costs the whole
         // warp's issue slots however few lanes take a move)
-        if (m == FULL || __popc(m) >= RL_REFILL_MIN) {
+        if (m == FULL || __popc(m) >= (kRegMask ? RL_REFILL_MIN : RL_REFILL_MIN_SMEM)) {
             if (state == 0) {
                 gi = (next + __popc(m & lt)) * nw + wi;
                 state = gi < n ? 1 : 0;
