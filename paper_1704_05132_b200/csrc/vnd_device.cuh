@@ -229,6 +229,9 @@ struct Slot {
 #ifndef RL_WALK_STEPS_SMEM
 #define RL_WALK_STEPS_SMEM 2
 #endif
+#ifndef RL_DENSE_PREV_TABLE
+#define RL_DENSE_PREV_TABLE 1
+#endif
 #ifndef RL_REFILL_MIN_SMEM   // shared-memory rows, two walk steps per iteration: measured
 #define RL_REFILL_MIN_SMEM 12   // C4 8 / 12 / 16 / 24: 109.8-111.3 / 109.5-110.4 / 110.6-111.9 / 120 ms
 #endif
@@ -1423,10 +1426,53 @@ __device__ inline void warp_argmin(C &best, int &key)
 // setup u of its candidate plan with entering X, the candidate's segment
 // costs so far in acc, and cd[u], cr[u+1] carried from the previous step
 // (each step loads one {cd, cr} pair and one {cpre, xin} pair).
+// Previous-setup table for the dense passes (N1/N2) of shared-memory rows:
+// pv[t] = last setup < t (0xffff if none), t <= T, written into the move-list
+// area (unused by dense passes).  A dense move's set-up then reads pv[a]
+// beside nx[a] instead of scanning the setup words backwards (one shared-
+// memory round trip instead of a data-dependent loop).  Lane chunks with a
+// warp max-scan of each chunk's last setup, like build_tables.
+__device__ inline void build_prev_table(const MaskSmem &mk, uint16_t *pv, int T, int lane)
+{
+    const int L = (T + 32) >> 5;   // periods 0..T
+    const int lo = lane * L, hi = min(lo + L, T + 1);
+    int last = -1;   // last setup in [lo, hi) (periods < T)
+    if (lo < hi) {
+        const int top = min(hi, T) - 1;
+        if (top >= lo) {
+            int w = top >> 5;
+            uint32_t bits = mk.bs[w] & (0xffffffffu >> (31 - (top & 31)));
+            const int wl = lo >> 5;
+            while (!bits && w > wl) {
+                --w;
+                bits = mk.bs[w];
+            }
+            const int f = bits ? (w << 5) + 31 - __clz(bits) : -1;
+            last = f >= lo ? f : -1;
+        }
+    }
+    int sm = last;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(FULL, sm, off);
+        if (lane >= off)
+            sm = max(sm, o);
+    }
+    int run = __shfl_up_sync(FULL, sm, 1);   // last setup before this chunk
+    if (lane == 0)
+        run = -1;
+    for (int t = lo; t < hi; ++t) {
+        pv[t] = (uint16_t)run;   // -1 -> 0xffff
+        if (t < T && mk.setup(t))
+            run = t;
+    }
+    __syncwarp();
+}
+
 template <typename V, typename C, typename Mask, bool Skip = false, int SB = 4>
 __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T,
                                   const ProductCosts<C> &pc, C S, int nbh, int n, int lane,
-                                  int wi, int nw, C &best, int &key)
+                                  int wi, int nw, C &best, int &key, bool pv_table = false)
 {
     const bool dense = nbh <= 2;
     const unsigned lt = (1u << lane) - 1;
@@ -1454,13 +1500,24 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
             ws_cur = 0;
         }
 #endif
-        if (state == 1) {
+#ifndef RL_SETUP_REPS
+#define RL_SETUP_REPS 1   // measurement only: > 1 repeats the (idempotent) move set-up
+#endif
+        const bool setup_now = state == 1;
+        for (int rep = 0; rep < RL_SETUP_REPS; ++rep)
+        if (setup_now) {
+            state = 1;
             RL_ASSERT(gi < n && gi < 4 * T);
             slot = dense ? gi : s.mv[gi];
             const MoveDesc d = slot_move(mk, nbh, slot, T);
             int a;
             pw = patch_of<V, C, Mask>(mk, d, a, b);
-            const int p = mk.prev(a);
+            int p;
+            if constexpr (!kRegMask && RL_DENSE_PREV_TABLE) {
+                p = dense && pv_table ? (int)(int16_t)s.mv[a] : mk.prev(a);   // build_prev_table
+            } else {
+                p = mk.prev(a);
+            }
             if (p >= 0) {   // the prefix before p is the base plan's
                 const XC<V, C> e = s.xc[p];
                 u = p;
@@ -1621,7 +1678,11 @@ __device__ inline PassResult scan_pass(const Slot<V, C, SB> &s, const Mask &mk, 
 #endif
     C best = S;
     int key = 0x7fffffff;
-    walk_moves<V, C, Mask, Skip>(s, mk, T, pc, S, nbh, n, lane, 0, 1, best, key);
+    const bool pv = std::is_same<Mask, MaskSmem>::value && RL_DENSE_PREV_TABLE && nbh <= 2;
+    if constexpr (std::is_same<Mask, MaskSmem>::value)
+        if (pv)
+            build_prev_table(mk, s.mv, T, lane);
+    walk_moves<V, C, Mask, Skip>(s, mk, T, pc, S, nbh, n, lane, 0, 1, best, key, pv);
     warp_argmin(best, key);
     PassResult res;
     res.improved = key != 0x7fffffff;
