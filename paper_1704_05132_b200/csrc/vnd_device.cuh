@@ -1504,8 +1504,9 @@ __device__ inline void walk_moves(const Slot<V, C, SB> &s, const Mask &mk, int T
 #define RL_SETUP_REPS 1   // measurement only: > 1 repeats the (idempotent) move set-up
 #endif
         const bool setup_now = state == 1;
-        for (int rep = 0; rep < RL_SETUP_REPS; ++rep)
-        if (setup_now) {
+        for (int rep = 0; rep < RL_SETUP_REPS; ++rep) {
+            if (!setup_now)
+                break;
             state = 1;
             RL_ASSERT(gi < n && gi < 4 * T);
             slot = dense ? gi : s.mv[gi];
