@@ -174,3 +174,57 @@ def test_merge_shards_equals_unsharded_reference(world):
         assert g_trace == trace.tolist() and tot["cost"] == cost
         assert tot["evals_reference"] == st["evals"] and tot["sweeps"] == st["sweeps"]
         assert tot["moves"] == st["moves"]
+
+
+def _gvns_long_worker(rank, world, port, names, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import json
+        from gvns_oracle import OracleRounds
+        from conftest import GOLDEN
+        from paper_1704_05132_b200.gvns import SolverConfig
+        from paper_1704_05132_b200.sharded import sharded_gvns
+        with open(os.path.join(GOLDEN, "gvns_long.json")) as f:
+            gold = json.load(f)
+        res = []
+        for name in names:
+            g = gold[name]
+            inst = generate_instance(GeneratorConfig(
+                products=g["products"], periods=g["periods"], seed=g["seed"],
+                setup_cost_range=tuple(g["setup_cost_range"])))
+            cfg = SolverConfig(t_max=1e9, k_max=5, k_vnd_max=4, workers=g["workers"], seed=5,
+                               max_rounds=g["rounds"])
+            r = sharded_gvns(inst, cfg, backend=OracleRounds(inst))
+            res.append((name, r.cost, r.rounds, r.shake_calls))
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_oracle_gvns_long_horizons_match_reference():
+    """The CPU restatement of the shake / worker rounds (oracle/gvns_oracle.py)
+    reproduces the live reference's round-capped gvns past the register rows
+    (T = 100, with int32 and int64 costs; tests/golden/gvns_long.json), the
+    workers split over 2 gloo ranks."""
+    import json
+    from conftest import GOLDEN
+    names = ["K40_T100_W2_R30", "K20_T100_c64_W2_R10"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gvns_long_worker, args=(r, 2, port, names, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    with open(os.path.join(GOLDEN, "gvns_long.json")) as f:
+        gold = json.load(f)
+    for rank in range(2):
+        for name, cost, rounds, shakes in got[rank]:
+            g = gold[name]
+            assert cost == g["cost"], name
+            assert rounds == g["rounds_done"] and shakes == g["shake_calls"], name
